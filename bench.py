@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Lloyd-iteration throughput (point-iterations / s) on B200, per BASELINE.json.
+
+A step is one Lloyd iteration over every point of the workload (assign or MTI
+filter/scan + accumulate, the cross-GPU exchange, finalize).  Default workload
+= BASELINE.json configs[1] ("c2"): n = 2,000,000, d = 32, k = 32, float64,
+mixture of 32 Gaussians, kmeans++ init, MTI pruning on.  W warm-up iterations
+run first (iteration 0 is the dense full pass), then exactly K iterations are
+timed with CUDA events on the launching stream, bracketed by barrier +
+synchronize, max over ranks.  The run keeps iterating after convergence (every
+timed step does the work of a real iteration of that run).
+
+Other keys: roofline (the step's dominant kernel, north-star definition:
+dense-equivalent n*k*d FMAs vs point bytes), roofline_k1 (the dense assign
+kernel timed on full passes), cpu_baseline (the oracle port of the reference
+on this host's cores, bounded sample), e2e (full kmeans() public-API calls from
+host numpy arrays, H2D/D2H included), clocks (nvidia-smi during the run).
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port in oracle/, pinned bit-for-bit to the reference package) on this
+host with all cores, on a bounded row sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "point-iterations/sec (n*iters/s)"
+UNIT = "point-iters/s"
+# rows of the bounded CPU sample per workload (about 10-30 s of oracle work on 8 cores)
+CPU_SAMPLE = {"c1": 200_000, "c2": 100_000, "c3": 1_000_000, "c4": 100_000, "c5": 20_000}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampler (start before the timed region, stop after)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        load = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(name: str, n: int | None):
+    from paper_1606_08905_b200 import synth
+    cfg = dict(synth.CONFIGS[name])
+    n = n or cfg["n"]
+    return cfg, n
+
+
+def cpu_port_run(name, cfg, n_sub, iters, threads):
+    """The oracle port (pinned to the reference) on n_sub rows; per-iteration wall times."""
+    from oracle import lloyd as O
+    m = cfg["data"](n_sub)
+    if m.dtype != np.float64:
+        m = m.astype(np.float64)
+    r = O.lloyd(m, cfg["k"], init=cfg["init"], seed=int(name[1:]), pruning=cfg["pruning"],
+                tolerance=cfg["tolerance"], max_iters=iters, threads=threads, force_iters=True)
+    return [s.wall_s for s in r.iterations], r
+
+
+def cpu_baseline(name, cfg, warmup, steps):
+    n_sub = min(CPU_SAMPLE[name], cfg["n"])
+    threads = os.cpu_count() or 1
+    walls, r = cpu_port_run(name, cfg, n_sub, warmup + steps, threads)
+    timed = walls[warmup:warmup + steps] or walls
+    value = n_sub * len(timed) / sum(timed)
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle/lloyd.py (restatement pinned bit-exact to numakmeans) on the first "
+                      f"{n_sub} rows of the {name} law, iterations {warmup}..{warmup + len(timed) - 1} "
+                      f"after the same init, {threads} threads"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, n = workload(args.config, args.n)
+    base = cpu_baseline(args.config, cfg, args.warmup, args.steps)
+    n_sub = min(CPU_SAMPLE[args.config], cfg["n"])
+    line = {
+        "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * n_sub / base["value"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "n_sample": n_sub, "k": cfg["k"], "init": cfg["init"],
+                   "pruning": cfg["pruning"]},
+        "impl": "reference", "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1606_08905_b200 as kb
+    from paper_1606_08905_b200 import _native
+    from paper_1606_08905_b200.parallel import LocalComm, TorchComm, shard_of
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    comm = LocalComm()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        comm = TorchComm()
+    name = args.config
+    cfg, n = workload(name, args.n)
+    k = cfg["k"]
+    seed = int(name[1:])
+    t_gen = time.perf_counter()
+    full = cfg["data"](n)
+    lo, hi = shard_of(n, rank, world)
+    host = np.ascontiguousarray(full[lo:hi], dtype=np.float64)
+    d = host.shape[1]
+    gen_s = time.perf_counter() - t_gen
+    dev_rows = torch.from_numpy(host).cuda()
+    torch.cuda.synchronize()
+
+    peaks = load_peaks()
+    mp = _native.measure_peaks(local_rank)
+    hbm_peak = peaks.get("hbm_gbs") or 6650.0
+    dfma_peak = mp["dfma_per_s"]
+
+    clocks = Clocks(local_rank)
+    total_iters = args.warmup + args.steps + 2
+    ecfg = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"], max_iters=total_iters,
+                           tolerance=cfg["tolerance"], device=local_rank)
+    t_init = time.perf_counter()
+    run = kb.Lloyd(dev_rows, ecfg, comm=comm, ignore_stop=True, device=local_rank)
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t_init
+    for _ in range(args.warmup):
+        run.step()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        run.local()
+        ev[i][1].record(stream)
+        run.exchange()
+        run.finish()
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = start.elapsed_time(stop)
+    local_ms = [a.elapsed_time(b) for a, b in ev]
+    if world > 1:
+        ms = max(comm.allgather_float(ms))
+    stats = run.ctx.stats()
+    desc = run.ctx.describe()
+    timed_stats = [s for s in stats if args.warmup <= s.t < args.warmup + args.steps]
+    comps = sum(s.dist_comps for s in timed_stats)
+    skips = sum(s.skips for s in timed_stats)
+    value = n * args.steps / (ms * 1e-3)
+
+    # dominant kernel: the local pass (K1 dense or K6/K7 MTI) + its CTA-partial merge
+    kern_s = statistics.mean(local_ms) * 1e-3
+    n_loc = hi - lo
+    flops = 2.0 * n_loc * k * d                      # dense-equivalent (north star definition)
+    bytes_ = 8.0 * n_loc * d                         # point bytes
+    t_fp = flops / (2 * dfma_peak)
+    t_hbm = bytes_ / (hbm_peak * 1e9)
+    if t_fp >= t_hbm:
+        roof = {"bound": "fp64", "achieved": flops / kern_s / 1e12, "peak": 2 * dfma_peak / 1e12,
+                "unit": "TFLOP/s", "peak_source": "measured in-run DFMA microbenchmark (knb_measure_peaks)"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_ / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = "mti_tile_kernel + reduce" if cfg["pruning"] else "dense_tile_kernel + reduce"
+    roof["kernel_ms"] = kern_s * 1e3
+    roof["work"] = "dense-equivalent 2*n*k*d flops and n*d*8 point bytes per launch; MTI skips are not discounted"
+    roof["computed_fraction"] = comps / max(1, n * k * len(timed_stats))
+    roof["skip_fraction"] = skips / max(1, n * len(timed_stats))
+
+    # the dense assign kernel alone: full passes against the current centroids
+    roof_k1 = None
+    if world == 1:
+        means, _, _, _ = run.ctx.centroids()
+        reps = 5
+        dcfg = kb.EngineConfig(k=k, init="given", initial_centroids=means, pruning=False, max_iters=reps + 2,
+                               device=local_rank)
+        dense = kb.Lloyd(dev_rows, dcfg, ignore_stop=True)
+        dense.local()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            dense.local()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        k1_s = e0.elapsed_time(e1) * 1e-3 / reps
+        dense.close()
+        roof_k1 = {"bound": "fp64" if t_fp >= t_hbm else "hbm", "kernel": "dense_tile_kernel + reduce",
+                   "kernel_ms": k1_s * 1e3, "dense_dp": desc["dense_dp"], "tma": desc["tma"]}
+        if t_fp >= t_hbm:
+            roof_k1.update(achieved=flops / k1_s / 1e12, peak=2 * dfma_peak / 1e12, unit="TFLOP/s")
+        else:
+            roof_k1.update(achieved=bytes_ / k1_s / 1e9, peak=hbm_peak, unit="GB/s")
+        roof_k1["frac"] = roof_k1["achieved"] / roof_k1["peak"]
+        roof_k1["hbm_GBps"] = bytes_ / k1_s / 1e9
+        roof_k1["fp64_TFLOPs"] = flops / k1_s / 1e12
+    run.close()
+
+    # end to end through the public API from host numpy (H2D + init + iterations + D2H)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        ecfg2 = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"],
+                                max_iters=cfg["max_iters"], tolerance=cfg["tolerance"], device=local_rank)
+        kb.kmeans(host[: min(n, 100_000)], ecfg2)  # warm-up (context + modules)
+        vals = []
+        for _ in range(args.e2e_reps):
+            t0 = time.perf_counter()
+            r = kb.kmeans(host, ecfg2)
+            el = time.perf_counter() - t0
+            vals.append((n * r.n_iterations / el, r.n_iterations, el))
+        best = max(vals)
+        e2e = {"value": best[0], "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
+               "d2h_bytes_per_step": int(n * 4 + 2 * k * d * 8 + 2 * k * 8),
+               "step": f"one kmeans(host ndarray, EngineConfig) call: {best[1]} iterations, "
+                       f"{best[2] * 1e3:.1f} ms wall incl. H2D, kmeans++/forgy init, D2H"}
+    clk = clocks.stop()
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        base = cpu_baseline(name, cfg, args.warmup, min(args.steps, 10))
+
+    launches_per_step = 4 + (1 if cfg["pruning"] else 0)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "n": n, "d": d, "k": k, "init": cfg["init"], "pruning": cfg["pruning"],
+                   "tolerance": cfg["tolerance"], "parallelism": f"row-shard x{world}",
+                   "l2": f"inputs {host.nbytes / 2**20:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
+                   if host.nbytes > 126e6 else "inputs smaller than L2 (launch-bound config)",
+                   "timed_iterations": f"{args.warmup}..{args.warmup + args.steps - 1} of one run"},
+        "roofline": roof, "roofline_k1": roof_k1, "cpu_baseline": base, "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps, "clocks": clk,
+        "setup": {"datagen_s": gen_s, "init_s": init_s, "dfma_peak_per_s": dfma_peak,
+                  "copy_GBps_measured": mp["copy_bytes_per_s"] / 1e9, "kernels": desc},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--n", type=int, default=None, help="override n (rows)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-reps", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: at least 3 warm-up steps
+    return run_reference(args) if args.impl == "reference" else run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,141 @@
+/* knor_b200.h -- C ABI of libknorb200.so, the B200 (sm_100a) Lloyd / MTI k-means path.
+ *
+ * The reference (numakmeans, knor arXiv 1606.08905) is a pure-Python package whose
+ * only public entry to this path is
+ *     kmeans(matrix, EngineConfig) -> KmeansResult           engine.py:489-500
+ * with no FFI of its own.  This header is the plain-pointer boundary that a ctypes
+ * (or cffi / C++) binding calls instead of the reference's in-process engine; the
+ * Python package paper_1606_08905_b200 is such a binding and mirrors the reference API.
+ * Each entry point names the reference code it replaces.
+ *
+ * Conventions: every function returns 0 on success or a negative KNB_E* code;
+ * knb_last_error() returns a thread-local message for the last failure.  A context
+ * (knb_ctx) owns one GPU's contiguous row shard [row_lo, row_lo + n_local) of an
+ * n_global x d matrix (partition_rows, matrix.py:196-213) and all per-point state;
+ * it is not thread-safe.  All work is enqueued on the context's CUDA stream; the
+ * functions that return host data synchronise it.  Host pointers are plain,
+ * C-contiguous arrays; device pointers are marked "dev".
+ */
+#ifndef KNOR_B200_H
+#define KNOR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNB_OK 0
+#define KNB_E_ARG (-1)     /* invalid argument            -> ValueError      */
+#define KNB_E_CUDA (-2)    /* CUDA runtime / driver error -> RuntimeError    */
+#define KNB_E_STATE (-3)   /* call out of order           -> RuntimeError    */
+#define KNB_E_COUNT (-4)   /* Sigma counts != n            -> RuntimeError (engine.py:378-380) */
+#define KNB_E_NOMEM (-5)   /* device allocation failed    -> MemoryError     */
+
+typedef struct knb_ctx knb_ctx;
+
+/* One row of IterationStats (engine.py:124-144). */
+typedef struct {
+  int64_t t;
+  int64_t reassignments;
+  double wcss;
+  int64_t dist_comps;
+  int64_t skips;
+  int64_t pruned_stale;
+  int64_t pruned_tight;
+  int32_t converged;
+  int32_t stop;
+  int64_t count_total;
+} knb_iter_stats;
+
+int knb_version(void);
+const char* knb_last_error(void);
+/* SM count, HBM bytes and compute capability of a device. */
+int knb_device_info(int device, int* sms, int64_t* hbm_bytes, int* cc_major, int* cc_minor);
+
+/* _Engine.__init__ (engine.py:212-254) for one shard: allocates assignment (int32, zeroed
+ * as at engine.py:226), and for pruning runs the upper bound (f64) and tight flag (u8)
+ * state (engine.py:227-235) plus running sums.  stream may be NULL (a private stream is
+ * created).  max_iters / tolerance are EngineConfig's (engine.py:63-72). */
+int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, int32_t d,
+               int32_t k, int32_t pruning, int32_t max_iters, double tolerance, void* stream,
+               knb_ctx** out);
+int knb_destroy(knb_ctx* ctx);
+
+/* Rows of the shard: copy from host (any pointer; pinned is faster) into a context-owned
+ * buffer, or attach caller-owned device rows.  Replaces _MemorySource (engine.py:162-191). */
+int knb_upload_rows(knb_ctx* ctx, const double* host, int64_t row_lo_local, int64_t rows);
+int knb_attach_rows(knb_ctx* ctx, const double* dev_rows);
+/* check_matrix's finite scan (matrix.py:46-48): *first_bad = first shard-local row with a
+ * NaN/inf, or -1. */
+int knb_check_finite(knb_ctx* ctx, int64_t* first_bad);
+
+/* Exchange vector: the per-shard accumulator that crosses GPUs once per iteration
+ * (sums k*d, counts k, sq k, 8 scalars: the merged Accumulator of centroids.py:55-107 plus
+ * the counters).  A caller doing multi-GPU all-reduces it in place between the *_local and
+ * *_finish calls; it may supply its own device buffer (e.g. a torch tensor). */
+int knb_exchange_len(knb_ctx* ctx, int64_t* len);
+int knb_set_exchange(knb_ctx* ctx, double* dev, int64_t len);
+int knb_exchange_ptr(knb_ctx* ctx, double** dev);
+
+/* init_centroids (centroids.py:131-189).  given: knb_set_centroids.  forgy / kmeans++ rows:
+ * knb_init_gather writes the requested global rows this shard owns into the exchange
+ * (zeros elsewhere; all-reduce across shards), then knb_init_from_exchange installs the
+ * first `count` rows as centroids 0..count-1.  random-partition: knb_init_partition_local
+ * accumulates the shard's rows by group label into the exchange, knb_init_partition_finish
+ * installs group means (empty group -> global mean) and resets the assignment to zero. */
+int knb_set_centroids(knb_ctx* ctx, const double* host_means);
+int knb_init_gather(knb_ctx* ctx, const int64_t* global_ids, int32_t count);
+int knb_init_from_exchange(knb_ctx* ctx, int32_t first, int32_t count);
+int knb_init_partition_local(knb_ctx* ctx, const int32_t* host_labels_local);
+int knb_init_partition_finish(knb_ctx* ctx);
+/* kmeans++ (centroids.py:175-189): d2 = min(d2, dist(x, c)^2) against the row in
+ * exchange[0:d]; returns the shard's sum of d2.  psum returns the shard's sum of d2/total;
+ * search returns the first shard-local row whose running sum of d2/total exceeds
+ * `threshold` (the sampled index of Generator.choice). */
+int knb_kpp_update(knb_ctx* ctx, int32_t first, double* local_total);
+int knb_kpp_psum(knb_ctx* ctx, double total, double* local_psum);
+int knb_kpp_search(knb_ctx* ctx, double total, double threshold, int64_t* local_idx);
+int knb_kpp_release(knb_ctx* ctx);
+
+/* One Lloyd iteration, split around the cross-GPU exchange:
+ *   local  -- engine._task_full / _task_pruned over every row of the shard (K1 or
+ *             K6/K7) and the fixed-order merge of CTA partials into the exchange;
+ *   finish -- the barrier action (engine.py:358-426): running sums, Sigma counts == n,
+ *             finalize, WCSS, stats row, convergence, MTI geometry.
+ * knb_iterate = local + finish + the stats row (single shard). */
+int knb_iter_local(knb_ctx* ctx);
+int knb_iter_finish(knb_ctx* ctx);
+int knb_iterate(knb_ctx* ctx, knb_iter_stats* out);
+/* Iterate a single-shard run until it stops (converged or max_iters), synchronising with
+ * the host only every `batch` iterations (the stop flag lives on the device). */
+int knb_run(knb_ctx* ctx, int32_t batch, int32_t* iterations_done);
+/* EngineConfig.validate_bounds test mode (engine.py:428-445), between local and finish:
+ * first row whose assignment != exhaustive argmin and first row whose bound is below its
+ * true distance (-1 when none). */
+int knb_validate(knb_ctx* ctx, int64_t* bad_assign_row, int64_t* bad_bound_row);
+
+/* Results: IterationStats rows so far, CentroidSet (centroids.py:15-52), assignments
+ * (KmeansResult.assignments, engine.py:480), MTI bounds (PruneState, pruning.py:64-81). */
+int knb_get_stats(knb_ctx* ctx, knb_iter_stats* out, int32_t max_count, int32_t* count);
+int knb_get_state(knb_ctx* ctx, int32_t* stop, int32_t* converged, int64_t* t, int32_t* count_error);
+int knb_get_centroids(knb_ctx* ctx, double* means, double* prev_means, int64_t* counts, double* drift);
+int knb_get_assignments(knb_ctx* ctx, int32_t* out, int64_t lo, int64_t count);
+int knb_get_bounds(knb_ctx* ctx, double* upper, uint8_t* tight);
+int knb_sync(knb_ctx* ctx);
+/* Benchmark hook: keep running full iterations after convergence (kmeans() never sets it). */
+int knb_set_ignore_stop(knb_ctx* ctx, int32_t on);
+/* Device bytes held by the context (the GPU analogue of KmeansResult.peak_state_bytes). */
+int knb_state_bytes(knb_ctx* ctx, int64_t* bytes);
+/* Which kernels the context uses: padded width (0 = generic), TMA on/off, grid sizes. */
+int knb_describe(knb_ctx* ctx, int32_t* dense_dp, int32_t* use_tma, int32_t* grid_dense, int32_t* grid_mti);
+
+/* Roofline denominators measured on the device: FP64 FMA rate (DFMA/s, 8 independent chains
+ * per thread over 8 CTAs/SM) and a 1 GiB device copy (read + write bytes/s). */
+int knb_measure_peaks(int device, double* dfma_per_s, double* copy_bytes_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KNOR_B200_H */

@@ -1,0 +1,746 @@
+// C ABI of libknorb200.so (declared in include/knor_b200.h).
+//
+// One knb_ctx = one GPU's row shard and all of its device state.  Everything is
+// enqueued on the context stream; only calls that hand data back to the host
+// synchronise.  No CPU fallback exists: every failure is reported.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/knor_b200.h"
+#include "kernels.h"
+
+using namespace knb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define KNB_CUDA(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? KNB_E_NOMEM : KNB_E_CUDA,              \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+constexpr size_t SMEM_LIMIT = 227 * 1024;
+
+}  // namespace
+
+struct knb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  long long n_global = 0, n_local = 0, row_lo = 0;
+  int d = 0, k = 0, pruning = 0, max_iters = 1;
+  double tolerance = 0.0;
+  int sms = 148;
+
+  const double* X = nullptr;
+  double* X_own = nullptr;
+  CUtensorMap tmap;
+  int use_tma = 0;
+
+  int DP = 0, DPm = 0, half_in_smem = 0;
+  int G_dense = 1, G_mti = 1;
+
+  int32_t* assign = nullptr;
+  double* upper = nullptr;
+  uint8_t* tight = nullptr;
+  double *means = nullptr, *prev = nullptr, *drift = nullptr, *counts = nullptr, *chn = nullptr,
+         *cn2 = nullptr, *half = nullptr, *half_min = nullptr, *wterm = nullptr, *run = nullptr,
+         *stage = nullptr;
+  double* exch = nullptr;
+  bool own_exch = true;
+  long long L = 0;
+  double* partials = nullptr;
+  int G_alloc = 0;
+  Ctrl* ctrl = nullptr;
+  IterStatsDev* stats = nullptr;
+  long long* bad = nullptr;
+  long long* ids_dev = nullptr;
+  int ids_cap = 0;
+  double* d2 = nullptr;
+  double* kpp_bs = nullptr;
+  double* kpp_scalar = nullptr;
+  long long* kpp_idx = nullptr;
+  int kpp_nblk = 0;
+
+  long long t_host = 0;
+  bool centroids_set = false;
+  long long bytes = 0;
+};
+
+namespace {
+
+template <typename T>
+int dev_alloc(knb_ctx* c, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? KNB_E_NOMEM : KNB_E_CUDA,
+                std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + " B): " + cudaGetErrorString(e));
+  c->bytes += (long long)(count * sizeof(T));
+  return KNB_OK;
+}
+
+FinalArgs final_args(knb_ctx* c) {
+  FinalArgs f;
+  f.k = c->k;
+  f.d = c->d;
+  f.n = c->n_global;
+  f.pruning = c->pruning;
+  f.exch = c->exch;
+  f.run = c->run;
+  f.means = c->means;
+  f.prev = c->prev;
+  f.drift = c->drift;
+  f.counts = c->counts;
+  f.chn = c->chn;
+  f.cn2 = c->cn2;
+  f.half = c->half;
+  f.half_min = c->half_min;
+  f.wterm = c->wterm;
+  f.ctrl = c->ctrl;
+  f.stats = c->stats;
+  return f;
+}
+
+// fresh run state: iteration 0, not stopped, assignment zero, running sums zero
+int reset_run(knb_ctx* c) {
+  Ctrl h;
+  std::memset(&h, 0, sizeof(h));
+  h.full_pass = 1;
+  h.max_iters = c->max_iters;
+  h.tolerance = c->tolerance;
+  KNB_CUDA(cudaMemcpyAsync(c->ctrl, &h, offsetof(Ctrl, cmax2), cudaMemcpyHostToDevice, c->stream));
+  KNB_CUDA(cudaMemsetAsync(c->assign, 0, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
+  if (c->pruning) KNB_CUDA(cudaMemsetAsync(c->run, 0, sizeof(double) * c->L, c->stream));
+  c->t_host = 0;
+  return KNB_OK;
+}
+
+int build_tmap(knb_ctx* c) {
+  c->use_tma = 0;
+  if (c->DP == 0 || (c->d & 1) || (reinterpret_cast<uintptr_t>(c->X) & 15) || c->n_local < 1 ||
+      c->n_local > 0x7fffffffLL)
+    return KNB_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      fn == nullptr || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return KNB_OK;  // cp.async loader instead (same layout)
+  }
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  const int PW = c->DP < 16 ? c->DP : 16;
+  const int R = dense_rows_per_tile(c->DP);
+  const int BR = R < 256 ? R : 256;
+  cuuint64_t gdim[2] = {(cuuint64_t)c->d, (cuuint64_t)c->n_local};
+  cuuint64_t gstride[1] = {(cuuint64_t)c->d * 8};
+  cuuint32_t box[2] = {(cuuint32_t)PW, (cuuint32_t)BR};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+  if (PW * 8 == 128) sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  else if (PW * 8 == 64) sw = CU_TENSOR_MAP_SWIZZLE_64B;
+  else if (PW * 8 == 32) sw = CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = encode(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(c->X), gdim, gstride,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS) c->use_tma = 1;
+  return KNB_OK;
+}
+
+int need_ready(knb_ctx* c, bool centroids) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (!c->X && c->n_local > 0) return fail(KNB_E_STATE, "rows not uploaded or attached");
+  if (centroids && !c->centroids_set) return fail(KNB_E_STATE, "centroids not initialised");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(KNB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return KNB_OK;
+}
+
+int launch_local(knb_ctx* c) {
+  const bool full = !c->pruning || c->t_host == 0;
+  if (full) {
+    DenseArgs a;
+    a.X = c->X;
+    a.n = c->n_local;
+    a.d = c->d;
+    a.k = c->k;
+    a.assign = c->assign;
+    a.upper = c->upper;
+    a.tight = c->tight;
+    a.mti_seed = c->pruning;
+    a.labels_only = 0;
+    a.means = c->means;
+    a.chn = c->chn;
+    a.partials = c->partials;
+    a.ctrl = c->ctrl;
+    a.use_tma = c->use_tma;
+    KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
+    KNB_CUDA(launch_reduce(c->partials, c->G_dense, c->L, c->exch, c->ctrl, c->stream));
+  } else {
+    MtiArgs a;
+    a.X = c->X;
+    a.n = c->n_local;
+    a.d = c->d;
+    a.k = c->k;
+    a.assign = c->assign;
+    a.upper = c->upper;
+    a.tight = c->tight;
+    a.means = c->means;
+    a.drift = c->drift;
+    a.half = c->half;
+    a.half_min = c->half_min;
+    a.partials = c->partials;
+    a.ctrl = c->ctrl;
+    a.half_in_smem = c->half_in_smem;
+    KNB_CUDA(launch_mti(a, c->DPm, c->G_mti, c->stream));
+    KNB_CUDA(launch_reduce(c->partials, c->G_mti, c->L, c->exch, c->ctrl, c->stream));
+  }
+  return KNB_OK;
+}
+
+int launch_finish(knb_ctx* c) {
+  FinalArgs f = final_args(c);
+  KNB_CUDA(launch_finalize(f, c->stream));
+  if (c->pruning) KNB_CUDA(launch_geometry(f, c->stream));
+  c->t_host += 1;
+  return KNB_OK;
+}
+
+int install_means(knb_ctx* c, const double* src_dev, int from_partition) {
+  FinalArgs f = final_args(c);
+  KNB_CUDA(launch_set_means(src_dev, c->k, c->d, f, from_partition, c->n_global, c->stream));
+  int rc = reset_run(c);
+  if (rc) return rc;
+  c->centroids_set = true;
+  return KNB_OK;
+}
+
+void to_host_stats(const IterStatsDev& s, knb_iter_stats* o) {
+  o->t = s.t;
+  o->reassignments = s.reassignments;
+  o->wcss = s.wcss;
+  o->dist_comps = s.dist_comps;
+  o->skips = s.skips;
+  o->pruned_stale = s.pruned_stale;
+  o->pruned_tight = s.pruned_tight;
+  o->converged = s.converged;
+  o->stop = s.stop;
+  o->count_total = s.count_total;
+}
+
+}  // namespace
+
+extern "C" {
+
+int knb_version(void) { return 1; }
+
+const char* knb_last_error(void) { return g_err.c_str(); }
+
+int knb_device_info(int device, int* sms, int64_t* hbm_bytes, int* cc_major, int* cc_minor) {
+  cudaDeviceProp p;
+  KNB_CUDA(cudaGetDeviceProperties(&p, device));
+  if (sms) *sms = p.multiProcessorCount;
+  if (hbm_bytes) *hbm_bytes = (int64_t)p.totalGlobalMem;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return KNB_OK;
+}
+
+int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, int32_t d, int32_t k,
+               int32_t pruning, int32_t max_iters, double tolerance, void* stream, knb_ctx** out) {
+  if (!out) return fail(KNB_E_ARG, "null out");
+  *out = nullptr;
+  if (n_global < 1 || n_local < 0 || row_lo < 0 || row_lo + n_local > n_global)
+    return fail(KNB_E_ARG, "bad shard geometry");
+  if (d < 1) return fail(KNB_E_ARG, "d must be >= 1");
+  if (k < 1) return fail(KNB_E_ARG, "k must be >= 1");
+  if (max_iters < 1) return fail(KNB_E_ARG, "max_iters must be >= 1");
+  if (!(tolerance >= 0.0)) return fail(KNB_E_ARG, "tolerance must be >= 0");
+  KNB_CUDA(cudaSetDevice(device));
+  knb_ctx* c = new knb_ctx();
+  std::memset(&c->tmap, 0, sizeof(c->tmap));
+  c->device = device;
+  c->n_global = n_global;
+  c->n_local = n_local;
+  c->row_lo = row_lo;
+  c->d = d;
+  c->k = k;
+  c->pruning = pruning ? 1 : 0;
+  c->max_iters = max_iters;
+  c->tolerance = tolerance;
+  int rc = KNB_OK;
+  auto bail = [&](int code) {
+    knb_destroy(c);
+    return code;
+  };
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return bail(fail(KNB_E_CUDA, "cudaGetDeviceProperties"));
+  c->sms = p.multiProcessorCount;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(KNB_E_CUDA, "cudaStreamCreate"));
+    c->own_stream = true;
+  }
+  // kernel selection
+  c->DP = dense_tile_dp(d);
+  if (c->DP && dense_tile_smem(c->DP, k) > SMEM_LIMIT) c->DP = 0;
+  c->DPm = dense_tile_dp(d);
+  c->half_in_smem = 0;
+  if (c->DPm) {
+    if ((size_t)k * k * 8 <= 64 * 1024 && mti_tile_smem(c->DPm, k, 1) <= SMEM_LIMIT) c->half_in_smem = 1;
+    else if (mti_tile_smem(c->DPm, k, 0) > SMEM_LIMIT) c->DPm = 0;
+  }
+  const long long nl = n_local > 0 ? n_local : 1;
+  {
+    const long long rows = dense_rows_per_tile(c->DP);
+    const long long tiles = (nl + rows - 1) / rows;
+    long long g = c->DP ? dense_tile_grid(c->DP, k, c->sms) : 4LL * c->sms;
+    c->G_dense = (int)(tiles < g ? tiles : g);
+  }
+  {
+    const long long rows = c->DPm ? 4LL * KNB_NT : KNB_NT;
+    const long long tiles = (nl + rows - 1) / rows;
+    long long g = c->DPm ? mti_tile_grid(c->DPm, k, c->half_in_smem, c->sms) : 4LL * c->sms;
+    c->G_mti = (int)(tiles < g ? tiles : g);
+  }
+  c->L = acc_len(k, d);
+  c->G_alloc = c->G_dense > c->G_mti ? c->G_dense : c->G_mti;
+  const size_t kd = (size_t)k * d;
+  if ((rc = dev_alloc(c, &c->assign, nl))) return bail(rc);
+  if (c->pruning) {
+    if ((rc = dev_alloc(c, &c->upper, nl))) return bail(rc);
+    if ((rc = dev_alloc(c, &c->tight, nl))) return bail(rc);
+    if ((rc = dev_alloc(c, &c->run, c->L))) return bail(rc);
+    if ((rc = dev_alloc(c, &c->half, (size_t)k * k))) return bail(rc);
+    if ((rc = dev_alloc(c, &c->half_min, k))) return bail(rc);
+    if (cudaMemsetAsync(c->tight, 0, nl, c->stream) != cudaSuccess) return bail(fail(KNB_E_CUDA, "memset"));
+  }
+  if ((rc = dev_alloc(c, &c->means, kd))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->prev, kd))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->stage, kd))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->drift, k))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->counts, k))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->chn, k))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->cn2, k))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->wterm, k))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->exch, c->L))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->partials, (size_t)c->G_alloc * c->L))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->ctrl, 1))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->stats, max_iters))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->bad, 2))) return bail(rc);
+  if (cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream) != cudaSuccess) return bail(fail(KNB_E_CUDA, "memset"));
+  if (cudaMemsetAsync(c->stats, 0, sizeof(IterStatsDev) * max_iters, c->stream) != cudaSuccess)
+    return bail(fail(KNB_E_CUDA, "memset"));
+  if ((rc = reset_run(c))) return bail(rc);
+  *out = c;
+  return KNB_OK;
+}
+
+int knb_destroy(knb_ctx* c) {
+  if (!c) return KNB_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
+                  c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->stats,
+                  c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (c->own_exch && c->exch) cudaFree(c->exch);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return KNB_OK;
+}
+
+int knb_upload_rows(knb_ctx* c, const double* host, int64_t lo, int64_t rows) {
+  if (!c || (!host && rows > 0)) return fail(KNB_E_ARG, "null argument");
+  if (lo < 0 || rows < 0 || lo + rows > c->n_local) return fail(KNB_E_ARG, "row range outside the shard");
+  KNB_CUDA(cudaSetDevice(c->device));
+  if (!c->X_own) {
+    int rc = dev_alloc(c, &c->X_own, (size_t)(c->n_local ? c->n_local : 1) * c->d);
+    if (rc) return rc;
+    c->X = c->X_own;
+    rc = build_tmap(c);
+    if (rc) return rc;
+  }
+  if (rows)
+    KNB_CUDA(cudaMemcpyAsync(c->X_own + lo * c->d, host, sizeof(double) * rows * c->d, cudaMemcpyHostToDevice,
+                             c->stream));
+  return KNB_OK;
+}
+
+int knb_attach_rows(knb_ctx* c, const double* dev) {
+  if (!c || !dev) return fail(KNB_E_ARG, "null argument");
+  KNB_CUDA(cudaSetDevice(c->device));
+  c->X = dev;
+  return build_tmap(c);
+}
+
+int knb_check_finite(knb_ctx* c, int64_t* first_bad) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  KNB_CUDA(cudaMemsetAsync(c->bad, 0xff, sizeof(long long), c->stream));
+  if (c->n_local) KNB_CUDA(launch_check_finite(c->X, c->n_local, c->d, c->bad, c->stream));
+  long long h;
+  KNB_CUDA(cudaMemcpyAsync(&h, c->bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (first_bad) *first_bad = h;  // -1 (all ones) when every value is finite
+  return KNB_OK;
+}
+
+int knb_exchange_len(knb_ctx* c, int64_t* len) {
+  if (!c || !len) return fail(KNB_E_ARG, "null argument");
+  *len = c->L;
+  return KNB_OK;
+}
+
+int knb_set_exchange(knb_ctx* c, double* dev, int64_t len) {
+  if (!c || !dev) return fail(KNB_E_ARG, "null argument");
+  if (len < c->L) return fail(KNB_E_ARG, "exchange buffer too small");
+  if (c->own_exch && c->exch) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->exch);
+    c->bytes -= (long long)(c->L * sizeof(double));
+  }
+  c->exch = dev;
+  c->own_exch = false;
+  return KNB_OK;
+}
+
+int knb_exchange_ptr(knb_ctx* c, double** dev) {
+  if (!c || !dev) return fail(KNB_E_ARG, "null argument");
+  *dev = c->exch;
+  return KNB_OK;
+}
+
+int knb_set_centroids(knb_ctx* c, const double* host) {
+  if (!c || !host) return fail(KNB_E_ARG, "null argument");
+  KNB_CUDA(cudaSetDevice(c->device));
+  KNB_CUDA(cudaMemcpyAsync(c->stage, host, sizeof(double) * c->k * c->d, cudaMemcpyHostToDevice, c->stream));
+  int rc = install_means(c, c->stage, 0);
+  if (rc) return rc;
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+int knb_init_gather(knb_ctx* c, const int64_t* ids, int32_t count) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  if (count < 1 || count > c->k || !ids) return fail(KNB_E_ARG, "gather count must be in [1, k]");
+  if (count > c->ids_cap) {
+    if (c->ids_dev) cudaFree(c->ids_dev);
+    c->ids_dev = nullptr;
+    if ((rc = dev_alloc(c, &c->ids_dev, c->k))) return rc;
+    c->ids_cap = c->k;
+  }
+  KNB_CUDA(cudaMemcpyAsync(c->ids_dev, ids, sizeof(long long) * count, cudaMemcpyHostToDevice, c->stream));
+  KNB_CUDA(cudaMemsetAsync(c->exch, 0, sizeof(double) * count * c->d, c->stream));
+  if (c->n_local)
+    KNB_CUDA(launch_gather_rows(c->X, c->n_local, c->row_lo, c->d, c->ids_dev, count, c->exch, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));  // ids is a caller buffer
+  return KNB_OK;
+}
+
+int knb_init_from_exchange(knb_ctx* c, int32_t first, int32_t count) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (first < 0 || count < 1 || first + count > c->k) return fail(KNB_E_ARG, "rows outside [0, k)");
+  KNB_CUDA(cudaSetDevice(c->device));
+  KNB_CUDA(cudaMemcpyAsync(c->stage + (size_t)first * c->d, c->exch, sizeof(double) * count * c->d,
+                           cudaMemcpyDeviceToDevice, c->stream));
+  if (first + count == c->k) {
+    int rc = install_means(c, c->stage, 0);
+    if (rc) return rc;
+  }
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+int knb_init_partition_local(knb_ctx* c, const int32_t* labels) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  if (!labels && c->n_local) return fail(KNB_E_ARG, "null labels");
+  rc = reset_run(c);  // also clears a stop flag left by an earlier run
+  if (rc) return rc;
+  if (c->n_local)
+    KNB_CUDA(cudaMemcpyAsync(c->assign, labels, sizeof(int32_t) * c->n_local, cudaMemcpyHostToDevice, c->stream));
+  DenseArgs a;
+  a.X = c->X;
+  a.n = c->n_local;
+  a.d = c->d;
+  a.k = c->k;
+  a.assign = c->assign;
+  a.upper = c->upper;
+  a.tight = c->tight;
+  a.mti_seed = 0;
+  a.labels_only = 1;
+  a.means = c->means;
+  a.chn = c->chn;
+  a.partials = c->partials;
+  a.ctrl = c->ctrl;
+  a.use_tma = c->use_tma;
+  KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
+  KNB_CUDA(launch_reduce(c->partials, c->G_dense, c->L, c->exch, c->ctrl, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));  // labels is a caller buffer
+  return KNB_OK;
+}
+
+int knb_init_partition_finish(knb_ctx* c) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  int rc = install_means(c, c->exch, 1);
+  if (rc) return rc;
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+static int kpp_buffers(knb_ctx* c) {
+  if (c->d2) return KNB_OK;
+  int rc;
+  c->kpp_nblk = (int)((c->n_local + KPP_BLOCK - 1) / KPP_BLOCK);
+  if (c->kpp_nblk < 1) c->kpp_nblk = 1;
+  if ((rc = dev_alloc(c, &c->d2, c->n_local ? c->n_local : 1))) return rc;
+  if ((rc = dev_alloc(c, &c->kpp_bs, c->kpp_nblk))) return rc;
+  if ((rc = dev_alloc(c, &c->kpp_scalar, 1))) return rc;
+  if ((rc = dev_alloc(c, &c->kpp_idx, 1))) return rc;
+  return KNB_OK;
+}
+
+int knb_kpp_update(knb_ctx* c, int32_t first, double* local_total) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  if ((rc = kpp_buffers(c))) return rc;
+  double h = 0.0;
+  if (c->n_local) {
+    KNB_CUDA(launch_kpp_update(c->X, c->n_local, c->d, c->exch, c->d2, first, c->kpp_bs, c->kpp_nblk, c->stream));
+    KNB_CUDA(launch_sum_blocks(c->kpp_bs, c->kpp_nblk, c->kpp_scalar, c->stream));
+    KNB_CUDA(cudaMemcpyAsync(&h, c->kpp_scalar, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (local_total) *local_total = h;
+  return KNB_OK;
+}
+
+int knb_kpp_psum(knb_ctx* c, double total, double* local_psum) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  if ((rc = kpp_buffers(c))) return rc;
+  double h = 0.0;
+  if (c->n_local) {
+    KNB_CUDA(launch_kpp_psums(c->d2, c->n_local, total, c->kpp_bs, c->kpp_nblk, c->stream));
+    KNB_CUDA(launch_sum_blocks(c->kpp_bs, c->kpp_nblk, c->kpp_scalar, c->stream));
+    KNB_CUDA(cudaMemcpyAsync(&h, c->kpp_scalar, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (local_psum) *local_psum = h;
+  return KNB_OK;
+}
+
+int knb_kpp_search(knb_ctx* c, double total, double threshold, int64_t* local_idx) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  if (!c->d2 || c->n_local < 1) return fail(KNB_E_STATE, "kmeans++ search without psum / rows");
+  KNB_CUDA(launch_kpp_search(c->d2, c->n_local, total, c->kpp_bs, c->kpp_nblk, threshold, c->kpp_idx, c->stream));
+  long long h;
+  KNB_CUDA(cudaMemcpyAsync(&h, c->kpp_idx, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (local_idx) *local_idx = h;
+  return KNB_OK;
+}
+
+int knb_kpp_release(knb_ctx* c) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->d2) {
+    cudaFree(c->d2);
+    c->bytes -= (long long)(sizeof(double) * (c->n_local ? c->n_local : 1));
+  }
+  c->d2 = nullptr;
+  return KNB_OK;
+}
+
+int knb_iter_local(knb_ctx* c) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  return launch_local(c);
+}
+
+int knb_iter_finish(knb_ctx* c) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  return launch_finish(c);
+}
+
+int knb_iterate(knb_ctx* c, knb_iter_stats* out) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  const long long t = c->t_host;
+  if ((rc = launch_local(c))) return rc;
+  if ((rc = launch_finish(c))) return rc;
+  IterStatsDev s;
+  Ctrl h;
+  KNB_CUDA(cudaMemcpyAsync(&h, c->ctrl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  if (t < c->max_iters)
+    KNB_CUDA(cudaMemcpyAsync(&s, c->stats + t, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (h.count_error)
+    return fail(KNB_E_COUNT, "iteration " + std::to_string(h.t - 1) + ": accumulator counts sum to " +
+                                 std::to_string(h.count_seen) + ", expected " + std::to_string(c->n_global));
+  if (out && t < c->max_iters) to_host_stats(s, out);
+  return KNB_OK;
+}
+
+int knb_run(knb_ctx* c, int32_t batch, int32_t* done) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  if (batch < 1) batch = 1;
+  Ctrl h;
+  for (;;) {
+    for (int b = 0; b < batch && c->t_host < c->max_iters; ++b) {
+      if ((rc = launch_local(c))) return rc;
+      if ((rc = launch_finish(c))) return rc;
+    }
+    KNB_CUDA(cudaMemcpyAsync(&h, c->ctrl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+    if (h.count_error)
+      return fail(KNB_E_COUNT, "accumulator counts sum to " + std::to_string(h.count_seen) + ", expected " +
+                                   std::to_string(c->n_global));
+    if ((h.stop && !h.ignore_stop) || c->t_host >= c->max_iters) break;
+  }
+  if (done) *done = (int32_t)h.t;
+  return KNB_OK;
+}
+
+int knb_validate(knb_ctx* c, int64_t* bad_assign, int64_t* bad_bound) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  if (!c->pruning) return fail(KNB_E_STATE, "validate needs a pruning run");
+  KNB_CUDA(cudaMemsetAsync(c->bad, 0xff, 2 * sizeof(long long), c->stream));
+  if (c->n_local)
+    KNB_CUDA(launch_validate(c->X, c->n_local, c->d, c->k, c->assign, c->upper, c->means, c->bad, c->stream));
+  long long h[2];
+  KNB_CUDA(cudaMemcpyAsync(h, c->bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (bad_assign) *bad_assign = h[0];
+  if (bad_bound) *bad_bound = h[1];
+  return KNB_OK;
+}
+
+int knb_get_stats(knb_ctx* c, knb_iter_stats* out, int32_t max_count, int32_t* count) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  Ctrl h;
+  KNB_CUDA(cudaMemcpyAsync(&h, c->ctrl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  long long nt = h.t < c->max_iters ? h.t : c->max_iters;
+  if (nt > max_count) nt = max_count;
+  std::vector<IterStatsDev> tmp((size_t)(nt > 0 ? nt : 1));
+  if (nt > 0) {
+    KNB_CUDA(cudaMemcpyAsync(tmp.data(), c->stats, sizeof(IterStatsDev) * nt, cudaMemcpyDeviceToHost, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  for (long long i = 0; i < nt; ++i) to_host_stats(tmp[i], out + i);
+  if (count) *count = (int32_t)nt;
+  return KNB_OK;
+}
+
+int knb_get_state(knb_ctx* c, int32_t* stop, int32_t* converged, int64_t* t, int32_t* count_error) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  Ctrl h;
+  KNB_CUDA(cudaMemcpyAsync(&h, c->ctrl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (stop) *stop = h.stop;
+  if (converged) *converged = h.converged;
+  if (t) *t = h.t;
+  if (count_error) *count_error = h.count_error;
+  return KNB_OK;
+}
+
+int knb_get_centroids(knb_ctx* c, double* means, double* prev, int64_t* counts, double* drift) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  const size_t kd = (size_t)c->k * c->d;
+  std::vector<double> cnt(c->k);
+  if (means) KNB_CUDA(cudaMemcpyAsync(means, c->means, kd * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (prev) KNB_CUDA(cudaMemcpyAsync(prev, c->prev, kd * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (drift) KNB_CUDA(cudaMemcpyAsync(drift, c->drift, (size_t)c->k * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (counts) KNB_CUDA(cudaMemcpyAsync(cnt.data(), c->counts, (size_t)c->k * 8, cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (counts)
+    for (int j = 0; j < c->k; ++j) counts[j] = (int64_t)cnt[j];
+  return KNB_OK;
+}
+
+int knb_get_assignments(knb_ctx* c, int32_t* out, int64_t lo, int64_t count) {
+  if (!c || (!out && count > 0)) return fail(KNB_E_ARG, "null argument");
+  if (lo < 0 || count < 0 || lo + count > c->n_local) return fail(KNB_E_ARG, "range outside the shard");
+  KNB_CUDA(cudaSetDevice(c->device));
+  if (count)
+    KNB_CUDA(cudaMemcpyAsync(out, c->assign + lo, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+int knb_get_bounds(knb_ctx* c, double* upper, uint8_t* tight) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (!c->pruning) return fail(KNB_E_STATE, "bounds exist only for pruning runs");
+  KNB_CUDA(cudaSetDevice(c->device));
+  if (upper && c->n_local)
+    KNB_CUDA(cudaMemcpyAsync(upper, c->upper, sizeof(double) * c->n_local, cudaMemcpyDeviceToHost, c->stream));
+  if (tight && c->n_local)
+    KNB_CUDA(cudaMemcpyAsync(tight, c->tight, c->n_local, cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+int knb_sync(knb_ctx* c) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+int knb_set_ignore_stop(knb_ctx* c, int32_t on) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  int v = on ? 1 : 0;
+  KNB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(c->ctrl) + offsetof(Ctrl, ignore_stop), &v, sizeof(int),
+                           cudaMemcpyHostToDevice, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
+int knb_state_bytes(knb_ctx* c, int64_t* bytes) {
+  if (!c || !bytes) return fail(KNB_E_ARG, "null argument");
+  *bytes = c->bytes;
+  return KNB_OK;
+}
+
+int knb_describe(knb_ctx* c, int32_t* dp, int32_t* tma, int32_t* gd, int32_t* gm) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (dp) *dp = c->DP;
+  if (tma) *tma = c->use_tma;
+  if (gd) *gd = c->G_dense;
+  if (gm) *gm = c->G_mti;
+  return KNB_OK;
+}
+
+}  // extern "C"

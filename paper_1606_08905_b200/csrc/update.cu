@@ -1,0 +1,259 @@
+// K3 stage 2 + K4 + K5 + K9: fixed-order reduction of CTA partials, centroid
+// finalize, WCSS/statistics, convergence test and MTI geometry -- the barrier
+// action of numakmeans (engine.py:358-426) on device.
+//
+//   reduce      sum the G CTA partials element by element in CTA order (fixed
+//               order -> bit-reproducible for a fixed grid; centroids.py:88-107
+//               merges per-task accumulators in task order for the same reason)
+//   finalize    pruned runs add the (all-reduced) deltas into running totals
+//               (engine.py:371-375); means = sums / counts for occupied
+//               clusters, empty clusters keep their previous mean; drift is the
+//               exact-recipe distance old -> new, 0 when empty
+//               (centroids.py:110-128); per-cluster WCSS terms for pruned runs
+//               (engine.py:385-388)
+//   stats       Sigma counts == n check (engine.py:378-380), WCSS, the
+//               IterationStats row, converged = reassigned <= tolerance, stop
+//               when converged or t + 1 >= max_iters (engine.py:413-416)
+//   geometry    half_dist[a][b] = 0.5 * d(c_a, c_b) (exact recipe) and the row
+//               minima off the diagonal, +inf for k == 1 (pruning.py:48-61)
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace knb {
+
+namespace {
+
+__global__ void reduce_kernel(const double* __restrict__ partials, int G, long long L,
+                              double* __restrict__ out, const Ctrl* ctrl) {
+  if (ctrl->stop && !ctrl->ignore_stop) return;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L;
+       e += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    int b = 0;
+    // four independent loads in flight, summed strictly in CTA order
+    for (; b + 4 <= G; b += 4) {
+      const double v0 = partials[(long long)b * L + e], v1 = partials[(long long)(b + 1) * L + e];
+      const double v2 = partials[(long long)(b + 2) * L + e], v3 = partials[(long long)(b + 3) * L + e];
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; b < G; ++b) s += partials[(long long)b * L + e];
+    out[e] = s;
+  }
+}
+
+// one warp per centroid
+__global__ void finalize_kernel(const FinalArgs f) {
+  if (f.ctrl->stop && !f.ctrl->ignore_stop) return;
+  const int k = f.k, d = f.d;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= k) return;
+  const long long kd = (long long)k * d;
+  double* sums = f.exch + (long long)j * d;
+  double cntj = f.exch[kd + j];
+  double sqj = f.exch[kd + k + j];
+  if (f.pruning) {  // running totals += this iteration's merged (deltas or full totals)
+    double* rs = f.run + (long long)j * d;
+    for (int e = lane; e < d; e += 32) rs[e] += sums[e];
+    __syncwarp();
+    if (lane == 0) {
+      f.run[kd + j] += cntj;
+      f.run[kd + k + j] += sqj;
+    }
+    __syncwarp();
+    sums = rs;
+    cntj = f.run[kd + j];
+    sqj = f.run[kd + k + j];
+  }
+  double* m = f.means + (long long)j * d;
+  double* pv = f.prev + (long long)j * d;
+  const bool occ = cntj > 0.0;
+  for (int e = lane; e < d; e += 32) {
+    const double old = m[e];
+    pv[e] = old;
+    if (occ) m[e] = sums[e] / cntj;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    f.drift[j] = occ ? sqrt(exact_sq_rt(m, pv, d)) : 0.0;
+    f.counts[j] = cntj;
+    const double n2 = exact_self_rt(m, d);
+    f.cn2[j] = n2;
+    f.chn[j] = -0.5 * n2;
+    if (f.pruning) {  // sq - ||sums||^2 / count, clamped at 0 (engine.py:385-388)
+      double s2 = 0.0;
+      for (int e = 0; e < d; ++e) s2 += sums[e] * sums[e];
+      const double term = sqj - s2 / cntj;
+      f.wterm[j] = occ ? (term > 0.0 ? term : 0.0) : 0.0;
+    }
+  }
+}
+
+__global__ void stats_kernel(const FinalArgs f) {
+  Ctrl* c = f.ctrl;
+  if (c->stop && !c->ignore_stop) return;
+  __shared__ double sw[32];
+  __shared__ double sc[32];
+  __shared__ double sm[32];
+  const int k = f.k, d = f.d, tid = threadIdx.x;
+  double cs = 0.0, ws = 0.0, mx = 0.0;
+  for (int j = tid; j < k; j += blockDim.x) {
+    cs += f.counts[j];
+    if (f.pruning) ws += f.wterm[j];
+    mx = fmax(mx, f.cn2[j]);
+  }
+  cs = warp_sum(cs);
+  ws = warp_sum(ws);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) { sc[tid >> 5] = cs; sw[tid >> 5] = ws; sm[tid >> 5] = mx; }
+  __syncthreads();
+  if (tid == 0) {
+    double C = 0.0, W = 0.0, M = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { C += sc[w]; W += sw[w]; M = fmax(M, sm[w]); }
+    const double* scal = f.exch + (long long)k * d + 2LL * k;
+    const long long t = c->t;
+    IterStatsDev st;
+    st.t = t;
+    st.reassignments = (long long)scal[S_REASSIGNED];
+    st.wcss = f.pruning ? W : scal[S_WCSS];
+    st.dist_comps = (long long)scal[S_COMPUTED];
+    st.skips = (long long)scal[S_SKIPS];
+    st.pruned_stale = (long long)scal[S_PSTALE];
+    st.pruned_tight = (long long)scal[S_PTIGHT];
+    st.count_total = (long long)C;
+    if ((long long)C != f.n) c->count_error = 1;
+    c->count_seen = (long long)C;
+    const int conv = (double)st.reassignments <= c->tolerance;
+    const int stop = conv || (t + 1 >= c->max_iters);
+    st.converged = conv;
+    st.stop = stop;
+    if (t < c->max_iters) f.stats[t] = st;
+    c->converged = conv;
+    c->stop = stop;
+    c->cmax2 = M;
+    c->full_pass = 0;
+    c->t = t + 1;
+  }
+}
+
+// one warp per row a of the half-distance matrix
+__global__ void geometry_kernel(const FinalArgs f) {
+  const Ctrl* c = f.ctrl;
+  if (c->stop && !c->ignore_stop) return;
+  const int k = f.k, d = f.d, lane = threadIdx.x & 31;
+  const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (a >= k) return;
+  const double* ca = f.means + (long long)a * d;
+  double mn = CUDART_INF;
+  for (int b = lane; b < k; b += 32) {
+    double h = 0.0;
+    if (b != a) {
+      // rowwise_distances(means[a+1:], means[a]) * 0.5 for a < b; the subtract's
+      // sign cannot change a square, so the matrix is exactly symmetric
+      const double* lo = a < b ? f.means + (long long)b * d : ca;
+      const double* hi = a < b ? ca : f.means + (long long)b * d;
+      h = sqrt(exact_sq_rt(lo, hi, d)) * 0.5;
+      mn = fmin(mn, h);
+    }
+    f.half[(long long)a * k + b] = h;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) f.half_min[a] = mn;  // +inf when k == 1
+}
+
+// Install initial centroids (given / forgy / kmeans++ rows, or random-partition
+// group sums) and derive the per-centroid quantities the kernels need.
+__global__ void set_means_kernel(const double* src, int k, int d, const FinalArgs f, int from_partition,
+                                 long long n) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= k) return;
+  double* m = f.means + (long long)j * d;
+  double* pv = f.prev + (long long)j * d;
+  if (!from_partition) {
+    for (int e = lane; e < d; e += 32) m[e] = pv[e] = src[(long long)j * d + e];
+  } else {
+    // src holds group sums/counts in the accumulator layout; an empty group takes
+    // the global mean (centroids.py:164-173)
+    const long long kd = (long long)k * d;
+    const double cj = src[kd + j];
+    for (int e = lane; e < d; e += 32) {
+      double v;
+      if (cj > 0.0) {
+        v = src[(long long)j * d + e] / cj;
+      } else {
+        double tot = 0.0;
+        for (int g = 0; g < k; ++g) tot += src[(long long)g * d + e];
+        v = tot / (double)n;
+      }
+      m[e] = pv[e] = v;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    f.drift[j] = 0.0;
+    f.counts[j] = 0.0;
+    const double n2 = exact_self_rt(m, d);
+    f.cn2[j] = n2;
+    f.chn[j] = -0.5 * n2;
+  }
+}
+
+__global__ void cmax_kernel(const FinalArgs f) {
+  __shared__ double sm[32];
+  double mx = 0.0;
+  for (int j = threadIdx.x; j < f.k; j += blockDim.x) mx = fmax(mx, f.cn2[j]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double M = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) M = fmax(M, sm[w]);
+    f.ctrl->cmax2 = M;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_reduce(const double* partials, int G, long long L, double* out, const Ctrl* ctrl,
+                          cudaStream_t s) {
+  long long blocks = (L + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  reduce_kernel<<<(int)blocks, 256, 0, s>>>(partials, G, L, out, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t s) {
+  const int wpb = 8;
+  finalize_kernel<<<(f.k + wpb - 1) / wpb, wpb * 32, 0, s>>>(f);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  stats_kernel<<<1, 1024, 0, s>>>(f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_geometry(const FinalArgs& f, cudaStream_t s) {
+  const int wpb = 8;
+  geometry_kernel<<<(f.k + wpb - 1) / wpb, wpb * 32, 0, s>>>(f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_means(const double* src, int k, int d, FinalArgs f, int from_partition, long long n,
+                             cudaStream_t s) {
+  const int wpb = 8;
+  set_means_kernel<<<(k + wpb - 1) / wpb, wpb * 32, 0, s>>>(src, k, d, f, from_partition, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cmax_kernel<<<1, 1024, 0, s>>>(f);
+  return cudaGetLastError();
+}
+
+}  // namespace knb

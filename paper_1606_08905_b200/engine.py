@@ -1,0 +1,343 @@
+"""GPU Lloyd's engine behind the reference API (numakmeans engine.py).
+
+``kmeans(matrix, EngineConfig) -> KmeansResult`` is the drop-in boundary
+(engine.py:489-500).  The reference's per-iteration super-phase -- workers
+assign and accumulate per task, then one barrier action merges, finalizes and
+tests convergence (engine.py:1-23) -- maps onto B200 as:
+
+    knb_iter_local   K1 dense assign+accumulate (full passes) or K6/K7 MTI
+                     filter/scan/deltas (pruned passes) over the shard's rows,
+                     then the fixed-order merge of CTA partials
+    exchange         all-reduce(sum) of the merged vector across GPUs (N > 1)
+    knb_iter_finish  running sums, Sigma counts == n, finalize, WCSS, stats row,
+                     convergence flag, MTI geometry -- all on device
+
+A single-GPU run without per-iteration host needs (assignment history,
+bound validation) queues ``batch`` iterations at a time and reads the device
+stop flag between batches; the iteration count and every statistic come from
+the device's own stats rows.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .centroids import INIT_METHODS, CentroidSet, device_init
+from .matrix import MatrixFormatError, check_shape
+from .parallel import LocalComm, shard_of
+
+MODES = ("im", "sem")
+POLICIES = ("numa", "fifo", "static")
+
+
+@dataclass
+class EngineConfig:
+    """Knobs for one clustering run -- the reference's fields and defaults (engine.py:59-96).
+
+    T, N, task_size and scheduler steer the reference's CPU threads; they are
+    validated identically and have no effect on GPU results.  ``device`` and
+    ``batch`` are additions: the CUDA device of a single-GPU run and how many
+    iterations are queued between host checks of the stop flag.
+    """
+
+    k: int
+    max_iters: int = 100
+    init: str = "forgy"
+    seed: int = 0
+    T: int = 1
+    N: int = 0
+    task_size: int = 8192
+    pruning: bool = True
+    mode: str = "im"
+    tolerance: float = 0
+    scheduler: str = "numa"
+    initial_centroids: np.ndarray | None = None
+    collect_assignments: bool = False
+    validate_bounds: bool = False
+    device: int | None = None
+    batch: int = 16
+
+    def validate(self) -> None:
+        if self.k < 1:
+            raise ValueError("k must be >= 1")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.task_size < 1:
+            raise ValueError("task_size must be >= 1")
+        if self.T < 1:
+            raise ValueError("T must be >= 1")
+        if self.N < 0:
+            raise ValueError("N must be >= 0")
+        if self.tolerance < 0:
+            raise ValueError("tolerance must be >= 0")
+        if self.init not in INIT_METHODS:
+            raise ValueError(f"unknown init {self.init!r}")
+        if self.mode not in MODES:
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.scheduler not in POLICIES:
+            raise ValueError(f"unknown scheduler {self.scheduler!r}")
+        if self.batch < 1:
+            raise ValueError("batch must be >= 1")
+
+
+@dataclass
+class IoDelta:
+    """I/O counters (engine.py:99-114); in-memory runs report none."""
+
+    bytes_requested: int = 0
+    bytes_read: int = 0
+    cache_hits: int = 0
+    cache_misses: int = 0
+    rows_elided: int = 0
+
+
+@dataclass
+class SchedCounters:
+    taken_local: int = 0
+    stolen_same_node: int = 0
+    stolen_remote: int = 0
+
+
+@dataclass
+class IterationStats:
+    """What one iteration did (engine.py:124-144).
+
+    ``wcss``: against the centroids current at assignment time for unpruned runs,
+    against the updated means (from the running sums) for pruned runs.  ``wall_s``
+    of a batched run is the batch's wall time divided evenly over its iterations.
+    """
+
+    t: int
+    reassignments: int
+    wcss: float
+    dist_comps: int
+    skips: int = 0
+    pruned_stale: int = 0
+    pruned_tight: int = 0
+    wall_s: float = 0.0
+    io: IoDelta | None = None
+    sched: SchedCounters = field(default_factory=SchedCounters)
+
+
+@dataclass
+class KmeansResult:
+    """engine.py:147-159.  For a sharded run ``assignments`` (and the history) hold the
+    calling rank's rows [row_lo, row_lo + len)."""
+
+    centroids: CentroidSet
+    assignments: np.ndarray
+    iterations: list[IterationStats]
+    converged: bool
+    io_totals: IoDelta | None = None
+    peak_state_bytes: int = 0
+    assignment_history: list[np.ndarray] | None = None
+    row_lo: int = 0
+    init_rows: list[int] | None = None
+
+    @property
+    def n_iterations(self) -> int:
+        return len(self.iterations)
+
+
+def _rows_of(matrix):
+    """numpy -> host rows (validated shape, f64); torch CUDA tensor -> device rows (zero copy)."""
+    try:
+        import torch  # noqa: F401
+        is_tensor = type(matrix).__module__.startswith("torch")
+    except ImportError:  # pragma: no cover
+        is_tensor = False
+    if is_tensor:
+        t = matrix
+        if t.dim() != 2:
+            raise MatrixFormatError(f"expected a 2-D matrix, got ndim={t.dim()}")
+        if t.shape[0] < 1 or t.shape[1] < 1:
+            raise MatrixFormatError(f"matrix must be at least 1x1, got {t.shape[0]}x{t.shape[1]}")
+        if not t.is_cuda:
+            return check_shape(t.numpy()), None
+        import torch
+        t = t.to(torch.float64).contiguous()
+        return None, t
+    return check_shape(matrix), None
+
+
+def kmeans(matrix, cfg: EngineConfig) -> KmeansResult:
+    """Cluster an in-memory matrix on one B200 (engine.py:489-500).
+
+    ``matrix`` is a host array (copied to HBM) or a CUDA tensor (used in place).
+    ``cfg.pruning`` selects the dense engine or the MTI engine; both produce the
+    reference's assignments every iteration.
+    """
+    if cfg.mode != "im":
+        raise ValueError("kmeans() runs in-memory; use kmeans_ondisk() for sem mode")
+    host, dev = _rows_of(matrix)
+    cfg.validate()
+    return _run(host, dev, cfg, LocalComm(), device=cfg.device)
+
+
+def kmeans_sharded(local_rows, cfg: EngineConfig, comm, n_global: int | None = None,
+                   device: int | None = None, context_cls=None) -> KmeansResult:
+    """One process per GPU: each rank passes ITS contiguous row shard, in rank order
+    (the partition_rows split, matrix.py:196-213, when built with ``shard_of``).
+
+    Rows never leave their GPU; one all-reduce of the accumulator vector per
+    iteration crosses NVLink.  Results are identical on every rank except
+    ``assignments``, which are the rank's own rows.
+    """
+    if cfg.mode != "im":
+        raise ValueError("kmeans() runs in-memory; use kmeans_ondisk() for sem mode")
+    host, dev = _rows_of(local_rows)
+    cfg.validate()
+    return _run(host, dev, cfg, comm, device=device, n_global=n_global, context_cls=context_cls)
+
+
+def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context_cls=None) -> KmeansResult:
+    rows = host if host is not None else dev
+    n_local, d = int(rows.shape[0]), int(rows.shape[1])
+    sizes = comm.allgather_int(n_local)
+    if n_global is not None and int(n_global) != sum(sizes):
+        raise ValueError(f"shards hold {sum(sizes)} rows, expected n_global={n_global}")
+    n = sum(sizes)
+    row_lo = sum(sizes[:comm.rank])
+    k = cfg.k
+    if device is None:
+        device = dev.device.index if dev is not None else 0
+    stream = None
+    if dev is not None or comm.world > 1:
+        import torch
+        with torch.cuda.device(device):
+            stream = torch.cuda.current_stream().cuda_stream
+    cls = context_cls or _native.Context
+    ctx = cls(device, n, n_local, row_lo, d, k, cfg.pruning, cfg.max_iters, cfg.tolerance, stream)
+    try:
+        exch = comm.make_exchange(ctx.exchange_len(), device)
+        if exch is not None:
+            ctx.set_exchange(exch.data_ptr(), exch.numel())
+        if dev is not None:
+            ctx.attach(dev.data_ptr())
+        else:
+            ctx.upload(host)
+        bad = ctx.first_nonfinite_row()
+        bad_global = comm.allreduce_min_int(row_lo + bad if bad >= 0 else n)
+        if bad_global < n:
+            raise MatrixFormatError(f"non-finite value in row {bad_global}")
+        init_rows = device_init(ctx, comm, exch, cfg.init, k, cfg.seed, cfg.initial_centroids,
+                                n, row_lo, n_local, d)
+        history = [] if cfg.collect_assignments else None
+        walls: list[float] = []
+        batched = comm.world == 1 and history is None and not cfg.validate_bounds
+        if batched:
+            t0 = time.perf_counter()
+            done = ctx.run(cfg.batch)
+            el = time.perf_counter() - t0
+            walls = [el / max(done, 1)] * done
+        else:
+            for t in range(cfg.max_iters):
+                t0 = time.perf_counter()
+                ctx.iter_local()
+                comm.allreduce_exchange(exch)
+                if cfg.validate_bounds and cfg.pruning:
+                    ba, bb = ctx.validate()
+                    ba = comm.allreduce_max_int(1 if ba >= 0 else 0)
+                    bb = comm.allreduce_max_int(1 if bb >= 0 else 0)
+                    if ba:
+                        raise AssertionError(f"iteration {t}: stored assignment differs from exhaustive argmin")
+                    if bb:
+                        raise AssertionError(f"iteration {t}: upper bound below true distance")
+                ctx.iter_finish()
+                st = ctx.state()
+                if st["count_error"]:
+                    raise RuntimeError(f"iteration {t}: accumulator counts sum to a value other than {n}")
+                if history is not None:
+                    history.append(ctx.assignments())
+                walls.append(time.perf_counter() - t0)
+                if st["stop"]:
+                    break
+        rows_stats = ctx.stats()
+        state = ctx.state()
+        if state["count_error"]:
+            raise RuntimeError(f"accumulator counts sum to a value other than {n}")
+        means, prev, counts, drift = ctx.centroids()
+        its = [IterationStats(t=int(s.t), reassignments=int(s.reassignments), wcss=float(s.wcss),
+                              dist_comps=int(s.dist_comps), skips=int(s.skips),
+                              pruned_stale=int(s.pruned_stale), pruned_tight=int(s.pruned_tight),
+                              wall_s=walls[i] if i < len(walls) else 0.0)
+               for i, s in enumerate(rows_stats)]
+        assignments = ctx.assignments()
+        peak = ctx.state_bytes()
+        return KmeansResult(
+            centroids=CentroidSet(means=means, prev_means=prev, counts=counts, drift=drift),
+            assignments=assignments,
+            iterations=its,
+            converged=bool(state["converged"]),
+            io_totals=None,
+            peak_state_bytes=peak,
+            assignment_history=history,
+            row_lo=row_lo,
+            init_rows=init_rows,
+        )
+    finally:
+        ctx.close()
+
+
+class Lloyd:
+    """Stepwise handle on one run (benchmarks, step-wise checks): rows stay resident,
+    ``step()`` runs exactly one iteration (local pass, exchange, finish).  With a
+    ``comm`` each rank passes its own row shard, as in ``kmeans_sharded``."""
+
+    def __init__(self, rows, cfg: EngineConfig, comm=None, ignore_stop: bool = False,
+                 device: int | None = None):
+        cfg.validate()
+        self.comm = comm or LocalComm()
+        host, dev = _rows_of(rows)
+        r = host if host is not None else dev
+        self.n_local, self.d = int(r.shape[0]), int(r.shape[1])
+        sizes = self.comm.allgather_int(self.n_local)
+        self.n = sum(sizes)
+        self.row_lo = sum(sizes[:self.comm.rank])
+        self.cfg = cfg
+        if device is None:
+            device = cfg.device if cfg.device is not None else (dev.device.index if dev is not None else 0)
+        self.device = device
+        stream = None
+        if dev is not None or self.comm.world > 1:
+            import torch
+            with torch.cuda.device(device):
+                stream = torch.cuda.current_stream().cuda_stream
+        self.ctx = _native.Context(device, self.n, self.n_local, self.row_lo, self.d, cfg.k, cfg.pruning,
+                                   cfg.max_iters, cfg.tolerance, stream)
+        self._dev = dev
+        self.exch = self.comm.make_exchange(self.ctx.exchange_len(), device)
+        if self.exch is not None:
+            self.ctx.set_exchange(self.exch.data_ptr(), self.exch.numel())
+        if dev is not None:
+            self.ctx.attach(dev.data_ptr())
+        else:
+            self.ctx.upload(host)
+        self.init_rows = device_init(self.ctx, self.comm, self.exch, cfg.init, cfg.k, cfg.seed,
+                                     cfg.initial_centroids, self.n, self.row_lo, self.n_local, self.d)
+        if ignore_stop:
+            self.ctx.set_ignore_stop(True)
+
+    def local(self) -> None:
+        self.ctx.iter_local()
+
+    def exchange(self) -> None:
+        self.comm.allreduce_exchange(self.exch)
+
+    def finish(self) -> None:
+        self.ctx.iter_finish()
+
+    def step(self) -> None:
+        self.local()
+        self.exchange()
+        self.finish()
+
+    def sync(self) -> None:
+        self.ctx.sync()
+
+    def close(self) -> None:
+        self.ctx.close()

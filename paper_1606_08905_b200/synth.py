@@ -1,0 +1,95 @@
+"""Seeded synthetic inputs standing in for the paper's datasets.
+
+The paper's Friendster eigenvector and RM/RU matrices are not
+available, so BASELINE.json's five configurations are generated here from a
+seed with the shapes, sizes and value distributions it states
+(SURVEY.md section 8(d)).  Host generation uses numpy's ``default_rng`` so the
+bytes are reproducible anywhere the same numpy runs; it is chunked, which
+leaves the stream unchanged (``rng.standard_normal((n, d))`` equals the
+concatenation of sequential chunk draws).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class MixtureSpec:
+    """A mixture of isotropic Gaussians.
+
+    centers: "uniform" in [lo, hi]^d or "normal" (N(0, I)); sigma: a constant
+    or a (lo, hi) range drawn per component; weights: None = equal, else the
+    Dirichlet concentration.
+    """
+
+    n: int
+    d: int
+    k: int
+    seed: int
+    centers: str = "uniform"
+    lo: float = -10.0
+    hi: float = 10.0
+    sigma: float | tuple[float, float] = 1.0
+    dirichlet: float | None = None
+    dtype: str = "float64"
+
+
+def mixture(spec: MixtureSpec, chunk_rows: int = 1 << 20, out: np.ndarray | None = None) -> np.ndarray:
+    rng = np.random.default_rng(spec.seed)
+    if spec.centers == "uniform":
+        centers = rng.uniform(spec.lo, spec.hi, (spec.k, spec.d))
+    elif spec.centers == "normal":
+        centers = rng.standard_normal((spec.k, spec.d))
+    else:
+        raise ValueError(f"unknown center law {spec.centers!r}")
+    if isinstance(spec.sigma, tuple):
+        sigma = rng.uniform(spec.sigma[0], spec.sigma[1], spec.k)
+    else:
+        sigma = np.full(spec.k, float(spec.sigma))
+    if spec.dirichlet is None:
+        w = np.full(spec.k, 1.0 / spec.k)
+    else:
+        w = rng.dirichlet(np.full(spec.k, float(spec.dirichlet)))
+    labels = rng.choice(spec.k, spec.n, p=w)
+    x = out if out is not None else np.empty((spec.n, spec.d), dtype=np.dtype(spec.dtype))
+    for a in range(0, spec.n, chunk_rows):
+        b = min(a + chunk_rows, spec.n)
+        lab = labels[a:b]
+        x[a:b] = centers[lab] + sigma[lab, None] * rng.standard_normal((b - a, spec.d))
+    return x
+
+
+def uniform(n: int, d: int, seed: int, chunk_rows: int = 1 << 20, dtype="float64") -> np.ndarray:
+    """i.i.d. U[0,1)^d = ``default_rng(seed).random((n, d))`` (config 4's law)."""
+    rng = np.random.default_rng(seed)
+    x = np.empty((n, d), dtype=dtype)
+    for a in range(0, n, chunk_rows):
+        b = min(a + chunk_rows, n)
+        x[a:b] = rng.random((b - a, d))
+    return x
+
+
+# BASELINE.json configs; seed = config index.
+CONFIGS = {
+    "c1": dict(n=200_000, d=16, k=8, init="forgy", pruning=False, max_iters=20, tolerance=0,
+               data=lambda n: mixture(MixtureSpec(n, 16, 8, 1, "uniform", -10, 10, 1.0, None))),
+    "c2": dict(n=2_000_000, d=32, k=32, init="kmeanspp", pruning=True, max_iters=100, tolerance=1e-6,
+               data=lambda n: mixture(MixtureSpec(n, 32, 32, 2, "uniform", -5, 5, (0.5, 2.0), 1.0))),
+    "c3": dict(n=66_000_000, d=8, k=10, init="forgy", pruning=True, max_iters=50, tolerance=0,
+               data=lambda n: mixture(MixtureSpec(n, 8, 10, 3, "uniform", -1, 1, 0.1, 0.5))),
+    "c4": dict(n=856_000_000, d=16, k=100, init="forgy", pruning=True, max_iters=20, tolerance=0,
+               data=lambda n: uniform(n, 16, 4)),
+    "c5": dict(n=10_000_000, d=256, k=1000, init="forgy", pruning=False, max_iters=10, tolerance=0,
+               data=lambda n: mixture(MixtureSpec(n, 256, 1000, 5, "normal", 0, 0, 0.3, None, "float32"))),
+}
+# Note: config 4's n rows are a prefix-consistent stream, so any n' < n gives the
+# first n' rows of the full matrix; the mixtures are not prefix-consistent in n
+# (labels are drawn before the noise), so sub-scale instances are their own datasets.
+
+
+def config_data(name: str, n: int | None = None) -> np.ndarray:
+    cfg = CONFIGS[name]
+    return cfg["data"](cfg["n"] if n is None else n)

@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference goldens and
+the CPU oracle.  Every test here needs a B200 and the built libknorb200.so."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1606_08905_b200 as kb
+from conftest import EPS_F64, assert_parity, golden, near_tie_rows
+from oracle import lloyd as O
+from oracle.golden_cases import CASES, case_cfg, case_data
+
+pytestmark = pytest.mark.gpu
+
+COUNTERS = ("reassignments", "dist_comps", "skips", "pruned_stale", "pruned_tight")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int32).tobytes()).hexdigest()
+
+
+def _cfg(name, **over):
+    c = case_cfg(name)
+    kw = dict(k=c["k"], init=c.get("init", "forgy"), seed=c.get("seed", 0), pruning=c.get("pruning", True),
+              max_iters=c.get("max_iters", 100), tolerance=c.get("tolerance", 0),
+              initial_centroids=c.get("initial"))
+    kw.update(over)
+    return kb.EngineConfig(**kw)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_gpu_matches_reference_golden(name):
+    g = golden(name)
+    m = case_data(name)
+    r = kb.kmeans(m, _cfg(name, collect_assignments=True))
+    counters = {key: g[key] for key in COUNTERS}
+    assert_parity(m.astype(np.float64), r, g["means"], g["assignments"], len(g["reassignments"]),
+                  want_prev=g["prev_means"], counters=counters, wcss=g["wcss"], what=name)
+    # every iteration's assignment vector, bit for bit
+    assert [_sha(h) for h in r.assignment_history] == list(g["history_sha"]), name
+    np.testing.assert_array_equal(r.centroids.counts, g["counts"])
+    assert r.converged == bool(g["converged"])
+
+
+@pytest.mark.parametrize("name", ["c1_full", "c3_mini", "kpp_pruned", "d33_pruned", "d65_dense"])
+def test_gpu_batched_run_equals_stepwise(name):
+    """The batched single-GPU loop (device stop flag) == the per-iteration loop."""
+    m = case_data(name)
+    a = kb.kmeans(m, _cfg(name, batch=7))
+    b = kb.kmeans(m, _cfg(name, collect_assignments=True))
+    assert a.n_iterations == b.n_iterations
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids.means, b.centroids.means)
+    for x, y in zip(a.iterations, b.iterations):
+        assert (x.reassignments, x.dist_comps, x.skips, x.wcss) == (y.reassignments, y.dist_comps, y.skips, y.wcss)
+
+
+def test_repeated_run_bit_identical():
+    """test_engine.py:92-101: same config -> identical bits (fixed-order reductions)."""
+    m = case_data("k50_pruned")
+    a = kb.kmeans(m, _cfg("k50_pruned"))
+    b = kb.kmeans(m, _cfg("k50_pruned"))
+    assert np.array_equal(a.centroids.means, b.centroids.means)
+    assert np.array_equal(a.assignments, b.assignments)
+    assert [s.wcss for s in a.iterations] == [s.wcss for s in b.iterations]
+
+
+def test_validate_bounds_mode():
+    """EngineConfig.validate_bounds runs the exhaustive-argmin + bound oracle each iteration."""
+    for name in ("mix_pruned", "d17_pruned", "k50_pruned"):
+        r = kb.kmeans(case_data(name), _cfg(name, validate_bounds=True, max_iters=12))
+        assert r.n_iterations >= 1
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pruned_equals_dense_every_iteration(seed):
+    """Reference criterion 1 (test_acceptance.py:56-81) on the GPU."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(1000, 30000))
+    d = int(rng.choice([2, 3, 8, 16, 32]))
+    k = int(rng.choice([2, 10, 50]))
+    m = kb.synth.mixture(kb.synth.MixtureSpec(n, d, 8, 100 + seed, "uniform", -6, 6, 1.0)) \
+        if seed % 2 else kb.synth.uniform(n, d, 100 + seed)
+    base = dict(k=k, seed=seed + 1, max_iters=8, collect_assignments=True)
+    p = kb.kmeans(m, kb.EngineConfig(pruning=True, **base))
+    q = kb.kmeans(m, kb.EngineConfig(pruning=False, **base))
+    assert p.n_iterations == q.n_iterations
+    for a, b in zip(p.assignment_history, q.assignment_history):
+        assert np.array_equal(a, b)
+    assert np.max(np.abs(p.centroids.means - q.centroids.means)) < 1e-9
+    o = O.lloyd(m, k, seed=seed + 1, max_iters=8, pruning=True)
+    assert_parity(m, p, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
+                  counters={key: [getattr(s, key) for s in o.iterations] for key in COUNTERS})
+
+
+def test_large_k_generic_path():
+    """k*d too large for shared memory -> generic kernels, same answers."""
+    m = kb.synth.uniform(6000, 16, 77)
+    cfg = dict(k=2000, seed=3, max_iters=3)
+    r = kb.kmeans(m, kb.EngineConfig(pruning=True, **cfg))
+    o = O.lloyd(m, 2000, seed=3, max_iters=3, pruning=True)
+    assert_parity(m, r, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
+                  counters={key: [getattr(s, key) for s in o.iterations] for key in COUNTERS})
+
+
+def test_torch_device_input_is_used_in_place():
+    import torch
+    m = case_data("kpp_pruned")
+    a = kb.kmeans(m, _cfg("kpp_pruned"))
+    t = torch.from_numpy(m).cuda()
+    b = kb.kmeans(t, _cfg("kpp_pruned"))
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids.means, b.centroids.means)
+
+
+def test_nonfinite_rejected_on_device():
+    m = kb.synth.uniform(5000, 4, 1)
+    m[3210, 2] = np.inf
+    with pytest.raises(kb.MatrixFormatError, match="row 3210"):
+        kb.kmeans(m, kb.EngineConfig(k=3))
+
+
+def test_forgy_k_gt_n_message():
+    with pytest.raises(ValueError, match="k <= n"):
+        kb.kmeans(np.random.default_rng(0).normal(size=(10, 2)), kb.EngineConfig(k=11, init="forgy"))
+
+
+def test_k1_and_more_workers_than_rows():
+    m = np.random.default_rng(1234).normal(size=(100, 3))
+    r = kb.kmeans(m, kb.EngineConfig(k=1, pruning=False))
+    assert r.n_iterations == 1 and r.converged
+    assert np.allclose(r.centroids.means[0], m.mean(axis=0))
+    m3 = np.random.default_rng(5).normal(size=(3, 2))
+    for pruning in (False, True):
+        r = kb.kmeans(m3, kb.EngineConfig(k=2, seed=1, T=8, pruning=pruning, max_iters=10))
+        assert r.converged and int(r.centroids.counts.sum()) == 3
+
+
+def test_wcss_non_increasing_and_counts():
+    for name in ("unif_dense", "unif_pruned", "mix_pruned", "c3_mini"):
+        r = kb.kmeans(case_data(name), _cfg(name))
+        w = [s.wcss for s in r.iterations]
+        assert all(b <= a * (1 + 1e-9) for a, b in zip(w, w[1:])), name
+        assert int(r.centroids.counts.sum()) == case_data(name).shape[0]
+
+
+def test_lloyd_step_api_matches_kmeans():
+    m = case_data("c4_mini")
+    cfg = _cfg("c4_mini", max_iters=6)
+    full = kb.kmeans(m, cfg)
+    s = kb.Lloyd(m, _cfg("c4_mini", max_iters=6))
+    for _ in range(6):
+        s.step()
+    s.sync()
+    means, _, _, _ = s.ctx.centroids()
+    assert np.array_equal(s.ctx.assignments(), full.assignments)
+    assert np.array_equal(means, full.centroids.means)
+    s.close()
+
+
+def _stepwise_sample_check(m, r, sample=20000, seed=0):
+    """Size-independent properties at full scale: sampled assignments equal the oracle's
+    argmin against the centroids they were made with (near-ties excepted); centroids are
+    the f64 means of the GPU's own assignment; Sigma counts == n."""
+    n, d = m.shape
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(n, size=min(sample, n), replace=False))
+    ids, _, _ = O.lloyd_step(m[rows], r.centroids.prev_means)
+    bad = rows[ids != r.assignments[rows]]
+    assert near_tie_rows(m, r.centroids.prev_means, bad, EPS_F64).size == bad.size
+    k = r.centroids.k
+    counts = np.bincount(r.assignments, minlength=k)
+    assert np.array_equal(counts, r.centroids.counts)
+    assert counts.sum() == n
+    sums = np.stack([np.bincount(r.assignments, weights=m[:, e], minlength=k) for e in range(d)], axis=1)
+    occ = counts > 0
+    want = r.centroids.means.copy()
+    want[occ] = sums[occ] / counts[occ, None]
+    scale = max(1.0, float(np.abs(want).max()))
+    assert float(np.abs(want - r.centroids.means).max()) / scale < 1e-9
+
+
+def test_config3_full_size_properties():
+    """Config 3 at its full n = 66M (4.2 GB): pruned == dense assignments after 6
+    iterations, sampled oracle argmin, exact means of the GPU's own assignment."""
+    cfg = kb.synth.CONFIGS["c3"]
+    m = cfg["data"](cfg["n"])
+    p = kb.kmeans(m, kb.EngineConfig(k=10, init="forgy", seed=3, pruning=True, max_iters=6))
+    q = kb.kmeans(m, kb.EngineConfig(k=10, init="forgy", seed=3, pruning=False, max_iters=6))
+    assert p.n_iterations == q.n_iterations == 6
+    assert np.array_equal(p.assignments, q.assignments)
+    assert [s.reassignments for s in p.iterations] == [s.reassignments for s in q.iterations]
+    _stepwise_sample_check(m, p)
+
+
+def test_config4_shape_sample():
+    """Config 4's law (U[0,1)^16, k=100) at 8M rows (1 GB): stepwise sampled parity."""
+    m = kb.synth.uniform(8_000_000, 16, 4)
+    r = kb.kmeans(m, kb.EngineConfig(k=100, init="forgy", seed=4, pruning=True, max_iters=3))
+    assert r.n_iterations == 3
+    _stepwise_sample_check(m, r, sample=5000)
