@@ -204,7 +204,7 @@ struct TileLayout {
   __device__ static __forceinline__ int elem_off(int r, int e, int R) {
     return chunk_off(r, e >> 1, R) + ((e & 1) << 3);
   }
-  static constexpr int tile_bytes(int R) { return R * DP * 8; }
+  __host__ __device__ static constexpr int tile_bytes(int R) { return R * DP * 8; }
 };
 
 // ------------------------------------------------------------------ PTX bits

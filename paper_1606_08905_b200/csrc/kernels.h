@@ -61,6 +61,10 @@ struct FinalArgs {
 };
 
 // kernel selection helpers
+int dense_mma_dp(int d);
+size_t dense_mma_smem(int DP, int k);
+int dense_mma_rows();
+cudaError_t launch_dense_mma(const CUtensorMap* tmap, const DenseArgs& a, int DP, int grid, cudaStream_t s);
 int dense_tile_dp(int d);                       // padded dim for the register path, 0 = generic
 size_t dense_tile_smem(int DP, int k);
 size_t mti_tile_smem(int DP, int k, int half_in_smem);

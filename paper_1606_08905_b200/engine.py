@@ -143,6 +143,16 @@ class KmeansResult:
         return len(self.iterations)
 
 
+def torch_stream(device: int) -> int:
+    """Handle of torch's current stream on ``device`` for the C ABI; torch's default
+    stream reports 0, which is passed as cudaStreamLegacy (0x1) so the library does
+    not create a private stream."""
+    import torch
+    with torch.cuda.device(device):
+        h = torch.cuda.current_stream().cuda_stream
+    return h or 1
+
+
 def _rows_of(matrix):
     """numpy -> host rows (validated shape, f64); torch CUDA tensor -> device rows (zero copy)."""
     try:
@@ -206,10 +216,8 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
     if device is None:
         device = dev.device.index if dev is not None else 0
     stream = None
-    if dev is not None or comm.world > 1:
-        import torch
-        with torch.cuda.device(device):
-            stream = torch.cuda.current_stream().cuda_stream
+    if dev is not None or getattr(comm, "cuda", False):
+        stream = torch_stream(device)  # NCCL orders its all-reduce after torch's current stream
     cls = context_cls or _native.Context
     ctx = cls(device, n, n_local, row_lo, d, k, cfg.pruning, cfg.max_iters, cfg.tolerance, stream)
     try:
@@ -303,10 +311,8 @@ class Lloyd:
             device = cfg.device if cfg.device is not None else (dev.device.index if dev is not None else 0)
         self.device = device
         stream = None
-        if dev is not None or self.comm.world > 1:
-            import torch
-            with torch.cuda.device(device):
-                stream = torch.cuda.current_stream().cuda_stream
+        if dev is not None or getattr(self.comm, "cuda", False):
+            stream = torch_stream(device)
         self.ctx = _native.Context(device, self.n, self.n_local, self.row_lo, self.d, cfg.k, cfg.pruning,
                                    cfg.max_iters, cfg.tolerance, stream)
         self._dev = dev
