@@ -123,13 +123,13 @@ int dense_tile_dp(int d) { return dense_mma_dp(d); }
 
 int dense_rows_per_tile(int DP) { return DP ? dense_mma_rows() : KNB_NT; }
 
-size_t dense_tile_smem(int DP, int k) { return dense_mma_smem(DP, k); }
+size_t dense_tile_smem(int DP, int k, int d) { return dense_mma_smem(DP, k, d); }
 
-int dense_tile_grid(int DP, int k, int sms) {
-  const size_t sm = dense_tile_smem(DP, k);
+int dense_tile_grid(int DP, int k, int d, int sms) {
+  const size_t sm = dense_tile_smem(DP, k, d);
   int per = (int)((227u * 1024u) / (sm + 1024));
   if (per < 1) per = 1;
-  if (per > 2) per = 2;  // register-bound at 1-2 CTAs of 256 threads
+  if (per > 2) per = 2;  // register-bound: at most two CTAs' warps per SM
   return sms * per;
 }
 

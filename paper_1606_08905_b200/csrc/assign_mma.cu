@@ -4,32 +4,37 @@
 // Replaces numakmeans engine._task_full (engine.py:285-319) and the streaming
 // nearest-centroid scan it calls (distance.py:94-116).
 //
-// Why DMMA: the contraction s = X C^T is a small dense GEMM per tile.  On B200 the
-// FP64 tensor path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) and the vector FP64 FMA
-// pipe have the same peak (measured 18.5 vs 18.2 T FMA/s, tools/microbench.cu), but a
-// DMMA does 256 FMAs from register fragments, whereas vector DFMA needs a centroid
-// operand per FMA from a warp-uniform LDS (measured 0.45 LDS.128 / clk / SM), which
-// caps the vector kernel near a quarter of peak.  tcgen05 has no f64 kind.
+// Why DMMA: the contraction s = X C^T is a small dense GEMM per block of rows.  On
+// B200 the FP64 tensor path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) and the vector
+// FP64 FMA pipe have the same peak (measured 18.5 vs 18.2 T FMA/s,
+// tools/microbench.cu), but a DMMA does 256 FMAs from register fragments, whereas
+// vector DFMA needs a warp-uniform centroid operand per FMA from shared memory
+// (measured 0.45 LDS.128 / clk / SM), which caps it near a quarter of peak.
+// tcgen05 has no f64 kind.
 //
-// Tile: a CTA of 8 warps owns 256 rows; each warp computes a 32-row x 32-centroid
-// block as 4 x 4 DMMA tiles over d/4 k-steps.  Point fragments come from the
-// swizzled TMA tile (conflict-free), centroid fragments from a shared-memory copy
-// pre-permuted into fragment order, and each accumulator starts at -||c_j||^2 / 2,
-// so the tensor core produces s_ij = x_i.c_j - ||c_j||^2/2 directly (argmax s ==
-// argmin distance).  The epilogue folds 8 columns per lane into a running best /
-// argbest plus the near-tie flag (integer ops only), then combines the 4 lanes of
-// each row quad with shuffles.  A point is certified when no other centroid scored
-// within tol = (8d+32) 2^-53 (||x||^2 + max||c||^2) of the winner -- a bound on the
-// rounding of both this contraction (any summation order) and the reference's
-// subtract-square recipe -- so the certified winner is exactly the reference's
-// argmin; uncertified points (near ties) are re-ranked with the exact recipe.  The
-// winner's distance is recomputed with the exact recipe (bit-identical to the
-// oracle on the reference's BLAS tree).
+// Warp-independent pipelines: every warp owns a strided sequence of 32-row blocks
+// and streams them through its own NS-stage buffer with its own 2-D TMA loads
+// (hardware-swizzled 32 x 16-double boxes) and mbarriers, so warps never wait for
+// each other inside the main loop and one warp's epilogue overlaps another's DMMA.
 //
-// Accumulation: per 32-row group one member mask per cluster (match.any), then
-// thread (dim e, group g) owns clusters j = g mod NG and adds members' values in
-// row order into CTA-private shared-memory sums -- deterministic, no atomics.  One
-// partial per CTA leaves for the fixed-order reduction (update.cu).
+// Per block: a warp computes 32 rows x up to 32 centroids per step as 4 x 4 DMMA
+// tiles over d/4 k-steps.  Centroid fragments come from a shared-memory copy
+// pre-permuted into fragment order and each accumulator starts at -||c_j||^2 / 2,
+// so the tensor core emits s_ij = x_i.c_j - ||c_j||^2/2 (argmax s == argmin
+// distance).  The epilogue keeps a running best / argbest and a near-tie flag
+// (integer ops), then merges the 4 lanes of each row quad.  A point is certified
+// when no other centroid scored within tol = (8d+32) 2^-53 (||x||^2 + max||c||^2)
+// of the winner -- a bound on the rounding of this contraction (any order) and of
+// the reference's subtract-square recipe -- so the certified winner is exactly the
+// reference's argmin; near ties are re-ranked with the exact recipe, and the
+// winner's distance is recomputed with it (bit-identical to the oracle on the
+// reference's BLAS tree).
+//
+// Accumulation is warp-local and deterministic: a 15-step bitonic shuffle sort
+// orders the block's 32 rows by (cluster, row); the warp then walks the sorted
+// rows with lanes = dims, adds each cluster segment in registers and flushes it
+// into the warp's private shared-memory sums.  At the end the CTA adds its warps'
+// sums in warp order into one partial for the fixed-order reduction (update.cu).
 #include <cuda.h>
 #include <math_constants.h>
 
@@ -40,30 +45,34 @@ namespace knb {
 
 namespace {
 
-constexpr int MR = KNB_NT;  // rows per tile: 32 per warp
+constexpr int BR = 32;  // rows per warp block
 
 __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-struct MmaSmem {
-  size_t xb0, xb1, bf, crow, chn, acc, cnt, sq, xsq, masks, mbar, red, total;
-  __host__ __device__ MmaSmem(int DP, int k) {
+__host__ __device__ inline int stages_for(int DP) { return DP <= 8 ? 4 : 2; }
+
+// shared memory: [centroids: bf, crow, chn] [per warp: NS stages, mbar, acc, cnt, sq]
+struct WarpSmem {
+  size_t bf, crow, chn, warp0, stage_bytes, mbar_off, acc_off, cnt_off, sq_off, per_warp, red, total;
+  __host__ __device__ WarpSmem(int DP, int k, int d, int W) {
     const int kp = (k + 7) & ~7;
-    const size_t tile = (size_t)MR * DP * 8;
+    const int NS = stages_for(DP);
     size_t o = 0;
-    xb0 = o;  o += tile;
-    xb1 = o;  o += tile;
     bf = o;   o += (size_t)kp * DP * 8;
     crow = o; o += (size_t)kp * DP * 8;
     chn = o;  o += (size_t)kp * 8;
-    acc = o;  o += (size_t)k * DP * 8;
-    cnt = o;  o += (size_t)k * 8;
-    sq = o;   o += (size_t)k * 8;
-    xsq = o;  o += (size_t)MR * 8;
-    masks = o; o += (size_t)(MR / 32) * k * 4;
-    o = al(o, 16);
-    mbar = o; o += 16;
-    red = o;  o += KNB_WARPS * 4 * 8;
-    total = o;
+    red = o;  o += 32 * 4 * 8;
+    o = al(o, 1024);
+    warp0 = o;
+    stage_bytes = (size_t)BR * DP * 8;              // multiple of 1024 for DP >= 4
+    size_t w = (size_t)NS * stage_bytes;
+    mbar_off = w; w += (size_t)NS * 8;
+    w = al(w, 16);
+    acc_off = w;  w += (size_t)k * d * 8;
+    cnt_off = w;  w += (size_t)k * 8;
+    sq_off = w;   w += (size_t)k * 8;
+    per_warp = al(w, 1024);
+    total = warp0 + (size_t)W * per_warp;
   }
 };
 
@@ -83,7 +92,7 @@ __device__ __forceinline__ void score_update(double& best, int& bid, bool& flag,
   bid = better ? j : bid;
 }
 
-// Merge a disjoint partial (best, id, flag) from another lane of the same row.
+// merge a disjoint partial (best, id, flag) held by lane ^ lanemask
 __device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int tolhi, int lanemask) {
   const double ob = __shfl_xor_sync(0xffffffffu, best, lanemask);
   const int oi = __shfl_xor_sync(0xffffffffu, bid, lanemask);
@@ -97,31 +106,47 @@ __device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int 
   bid = other ? oi : bid;
 }
 
-template <int DP>
-__device__ __forceinline__ void issue_tile(const CUtensorMap* tmap, uint64_t* bar, unsigned char* dst,
-                                           long long tile, const DenseArgs& a, bool tma) {
-  using TL = TileLayout<DP>;
-  const long long row0 = tile * MR;
-  if (tma) {
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(bar, TL::tile_bytes(MR));
+// ascending bitonic sort of one 32-bit key per lane
+__device__ __forceinline__ unsigned warp_sort(unsigned key, int lane) {
 #pragma unroll
-      for (int p = 0; p < TL::NPANEL; ++p) tma_load_2d(dst + p * MR * TL::RB, tmap, bar, p * TL::PW, (int)row0);
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const unsigned other = __shfl_xor_sync(0xffffffffu, key, stride);
+      const bool up = size == 32 ? true : ((lane & size) == 0);
+      const bool lower = (lane & stride) == 0;
+      const unsigned lo = key < other ? key : other, hi = key < other ? other : key;
+      key = (lower == up) ? lo : hi;
+    }
+  }
+  return key;
+}
+
+template <int DP>
+__device__ __forceinline__ void load_block(const CUtensorMap* tmap, uint64_t* bar, unsigned char* dst, long long blk,
+                                           const DenseArgs& a, bool tma, int lane) {
+  using TL = TileLayout<DP>;
+  const long long row0 = blk * BR;
+  if (tma) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bar, TL::tile_bytes(BR));
+#pragma unroll
+      for (int p = 0; p < TL::NPANEL; ++p) tma_load_2d(dst + p * BR * TL::RB, tmap, bar, p * TL::PW, (int)row0);
     }
   } else {
-    const int rows = (int)(a.n - row0 < MR ? a.n - row0 : MR);
+    const int rows = (int)(a.n - row0 < BR ? a.n - row0 : BR);
     const int d = a.d;
     const double* src = a.X + row0 * d;
     if (((d & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0)) {
       const int hd = d >> 1;
-      for (int i = threadIdx.x; i < rows * hd; i += KNB_NT) {
+      for (int i = lane; i < rows * hd; i += 32) {
         const int r = i / hd, q = i - r * hd;
-        cp_async16(dst + TL::chunk_off(r, q, MR), src + 2LL * i);
+        cp_async16(dst + TL::chunk_off(r, q, BR), src + 2LL * i);
       }
     } else {
-      for (int i = threadIdx.x; i < rows * d; i += KNB_NT) {
+      for (int i = lane; i < rows * d; i += 32) {
         const int r = i / d, e = i - r * d;
-        cp_async8(dst + TL::elem_off(r, e, MR), src + i);
+        cp_async8(dst + TL::elem_off(r, e, BR), src + i);
       }
     }
     cp_async_commit();
@@ -132,98 +157,100 @@ template <int DP>
 __global__ void __launch_bounds__(KNB_NT, 1)
     dense_mma_kernel(const __grid_constant__ CUtensorMap tmap, const DenseArgs a) {
   using TL = TileLayout<DP>;
-  constexpr int KS = DP / 4;            // k-steps of 4 dims
-  constexpr bool ACACHE = DP <= 32;     // point fragments stay in registers
-  constexpr int RG = MR / 32;
+  constexpr int KS = DP / 4;         // k-steps of 4 dims
+  constexpr bool ACACHE = DP <= 32;  // point fragments stay in registers across centroid blocks
+  constexpr int NS = DP <= 8 ? 4 : 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
 
   const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
-  const MmaSmem L(DP, k);
-  unsigned char* const xb0 = smem + L.xb0;
-  unsigned char* const xb1 = smem + L.xb1;
+  const WarpSmem L(DP, k, d, W);
   double* bf = reinterpret_cast<double*>(smem + L.bf);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
   double* chn = reinterpret_cast<double*>(smem + L.chn);
-  double* acc = reinterpret_cast<double*>(smem + L.acc);
-  double* cnt = reinterpret_cast<double*>(smem + L.cnt);
-  double* sqa = reinterpret_cast<double*>(smem + L.sq);
-  double* xsq = reinterpret_cast<double*>(smem + L.xsq);
-  uint32_t* masks = reinterpret_cast<uint32_t*>(smem + L.masks);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.mbar);
   double* red = reinterpret_cast<double*>(smem + L.red);
+  unsigned char* wbase = smem + L.warp0 + (size_t)warp * L.per_warp;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + L.mbar_off);
+  double* acc = reinterpret_cast<double*>(wbase + L.acc_off);
+  double* cnt = reinterpret_cast<double*>(wbase + L.cnt_off);
+  double* sqa = reinterpret_cast<double*>(wbase + L.sq_off);
   const bool tma = a.use_tma != 0;
   const bool labels = a.labels_only != 0;
 
-  // centroids: row layout (exact recipe) and DMMA B-fragment order
+  // centroids: row layout (exact recipe) and B-fragment order
   //   bf[((q*KS + s)*32 + l)] = C[q*8 + l/4][s*4 + l%4]
-  for (int i = tid; i < kp * DP; i += KNB_NT) {
+  for (int i = tid; i < kp * DP; i += blockDim.x) {
     const int j = i / DP, e = i - j * DP;
     crow[i] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
-  }
-  for (int i = tid; i < kp * DP; i += KNB_NT) {
     const int l = i & 31, qs = i >> 5, q = qs / KS, s = qs - q * KS;
-    const int j = q * 8 + (l >> 2), e = s * 4 + (l & 3);
-    bf[i] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
+    const int jb = q * 8 + (l >> 2), eb = s * 4 + (l & 3);
+    bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
   }
-  for (int j = tid; j < kp; j += KNB_NT) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
-  for (int i = tid; i < k * DP; i += KNB_NT) acc[i] = 0.0;
-  for (int j = tid; j < k; j += KNB_NT) { cnt[j] = 0.0; sqa[j] = 0.0; }
+  for (int j = tid; j < kp; j += blockDim.x) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
+  for (int i = lane; i < k * d; i += 32) acc[i] = 0.0;
+  for (int j = lane; j < k; j += 32) { cnt[j] = 0.0; sqa[j] = 0.0; }
   if (!tma && d < DP) {  // cp.async never writes the padded columns: zero them once
-    for (int b = 0; b < 2; ++b)
-      for (int i = tid; i < MR * DP; i += KNB_NT) {
+    for (int s = 0; s < NS; ++s)
+      for (int i = lane; i < BR * DP; i += 32) {
         const int r = i / DP, e = i - r * DP;
-        if (e >= d) *reinterpret_cast<double*>((b ? xb1 : xb0) + TL::elem_off(r, e, MR)) = 0.0;
+        if (e >= d) *reinterpret_cast<double*>(wbase + s * L.stage_bytes + TL::elem_off(r, e, BR)) = 0.0;
       }
   }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
     fence_barrier_init();
-    if (tma) prefetch_tmap(&tmap);
+    if (tma && warp == 0) prefetch_tmap(&tmap);
   }
   __syncthreads();
 
   const double cmax2 = a.ctrl->cmax2;
   const double tolk = (8.0 * d + 32.0) * 1.1102230246251565e-16;  // (8d+32) * 2^-53
-  const long long ntiles = (a.n + MR - 1) / MR;
+  const long long nblk = (a.n + BR - 1) / BR;
+  const long long gw = (long long)blockIdx.x * W + warp, TW = (long long)gridDim.x * W;
   long long reassigned = 0, rows_done = 0;
   double wcss = 0.0;
-  uint32_t ph0 = 0u, ph1 = 0u;
-  int buf = 0;
-  if ((long long)blockIdx.x < ntiles) issue_tile<DP>(&tmap, &bar[0], xb0, blockIdx.x, a, tma);
 
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long next = tile + gridDim.x;
-    if (next < ntiles) issue_tile<DP>(&tmap, buf ? &bar[0] : &bar[1], buf ? xb0 : xb1, next, a, tma);
-    for (int i = tid; i < RG * k; i += KNB_NT) masks[i] = 0u;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (gw + s * TW < nblk) load_block<DP>(&tmap, &bar[s], wbase + s * L.stage_bytes, gw + s * TW, a, tma, lane);
+
+  int it = 0;
+  for (long long blk = gw; blk < nblk; blk += TW, ++it) {
+    const int s = it % NS;
+    unsigned char* tb = wbase + s * L.stage_bytes;
     if (tma) {
-      if (buf) { mbar_wait(&bar[1], ph1); ph1 ^= 1u; } else { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
+      mbar_wait(&bar[s], (uint32_t)((it / NS) & 1));
     } else {
-      if (next < ntiles) cp_async_wait_1(); else cp_async_wait_all();
+      // groups complete in order: allow the NS-1 younger groups to stay in flight
+      const long long left = (nblk - 1 - blk) / TW;  // blocks after this one
+      if (left >= NS - 1) {
+        if constexpr (NS == 4) asm volatile("cp.async.wait_group 3;" ::: "memory");
+        else asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        cp_async_wait_all();
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    const unsigned char* tb = buf ? xb1 : xb0;
-    const long long row0 = tile * MR;
-    // this lane's own point after the quad combine: row (t4 * 8 + g) of the warp's 32
-    const int my_r = warp * 32 + t4 * 8 + g;
+    const long long row0 = blk * BR;
+    const int my_r = t4 * 8 + g;  // the row this lane finishes after the quad combine
     const bool valid = row0 + my_r < a.n;
     int my_id = 0;
+    double my_sq = 0.0;
 
     if (!labels) {
-      // ---- point fragments: A[m][kk] = x[warp*32 + pg*8 + g][s*4 + t4]
+      // ---- point fragments: A[m][kk] = x[pg*8 + g][s*4 + t4]
       double afr[4][ACACHE ? KS : 1];
       double xn2[4];
 #pragma unroll
       for (int pg = 0; pg < 4; ++pg) {
-        const int r = warp * 32 + pg * 8 + g;
         double s2 = 0.0;
 #pragma unroll
-        for (int s = 0; s < KS; ++s) {
-          const double v = *reinterpret_cast<const double*>(tb + TL::elem_off(r, s * 4 + t4, MR));
-          if constexpr (ACACHE) afr[pg][s] = v;
+        for (int ks = 0; ks < KS; ++ks) {
+          const double v = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
+          if constexpr (ACACHE) afr[pg][ks] = v;
           s2 = fma(v, v, s2);
         }
         s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
@@ -240,7 +267,6 @@ __global__ void __launch_bounds__(KNB_NT, 1)
         bid[pg] = 0;
         flag[pg] = false;
       }
-      // ---- centroid blocks of up to 32 (4 n-tiles of 8)
 #pragma unroll 1
       for (int cb = 0; cb < ntile8; cb += 4) {
         const int nq = ntile8 - cb < 4 ? ntile8 - cb : 4;
@@ -253,17 +279,17 @@ __global__ void __launch_bounds__(KNB_NT, 1)
           for (int pg = 0; pg < 4; ++pg) { c[pg][q][0] = h.x; c[pg][q][1] = h.y; }
         }
 #pragma unroll
-        for (int s = 0; s < KS; ++s) {
+        for (int ks = 0; ks < KS; ++ks) {
           double av[4];
 #pragma unroll
           for (int pg = 0; pg < 4; ++pg) {
-            if constexpr (ACACHE) av[pg] = afr[pg][s];
-            else av[pg] = *reinterpret_cast<const double*>(tb + TL::elem_off(warp * 32 + pg * 8 + g, s * 4 + t4, MR));
+            if constexpr (ACACHE) av[pg] = afr[pg][ks];
+            else av[pg] = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (q < nq) {
-              const double bv = bf[(((cb + q) * KS + s) << 5) + lane];
+              const double bv = bf[(((cb + q) * KS + ks) << 5) + lane];
 #pragma unroll
               for (int pg = 0; pg < 4; ++pg) dmma(c[pg][q], av[pg], bv);
             }
@@ -281,38 +307,49 @@ __global__ void __launch_bounds__(KNB_NT, 1)
           }
         }
       }
-      // ---- combine the 4 lanes of each row quad
 #pragma unroll
       for (int pg = 0; pg < 4; ++pg) {
         combine(best[pg], bid[pg], flag[pg], tolhi[pg], 1);
         combine(best[pg], bid[pg], flag[pg], tolhi[pg], 2);
       }
-      // lane takes point group pg == t4 (row t4*8 + g)
       int id = bid[0];
       bool fl = flag[0];
+      double sb = best[0], xs = xn2[0];
 #pragma unroll
       for (int pg = 1; pg < 4; ++pg)
-        if (t4 == pg) { id = bid[pg]; fl = flag[pg]; }
-      // ---- exact recipe on the lane's own point
-      double x[DP];
+        if (t4 == pg) { id = bid[pg]; fl = flag[pg]; sb = best[pg]; xs = xn2[pg]; }
+      double nd2 = 0.0;  // squared nearest distance
+      if (fl || a.mti_seed) {
+        // exact recipe on the lane's own row: near-tie re-rank, or the MTI bound seed
+        double x[DP];
 #pragma unroll
-      for (int q2 = 0; q2 < DP / 2; ++q2) {
-        const double2 v = *reinterpret_cast<const double2*>(tb + TL::chunk_off(my_r, q2, MR));
-        x[2 * q2] = v.x;
-        x[2 * q2 + 1] = v.y;
-      }
-      double nd;
-      if (fl) {  // near tie: exact re-rank over every centroid, ascending, strict <
-        double bd = CUDART_INF;
-        int bi = 0;
-        for (int j = 0; j < k; ++j) {
-          const double dj = sqrt(exact_sq<DP>(x, crow + j * DP, d));
-          if (dj < bd) { bd = dj; bi = j; }
+        for (int q2 = 0; q2 < DP / 2; ++q2) {
+          const double2 v = *reinterpret_cast<const double2*>(tb + TL::chunk_off(my_r, q2, BR));
+          x[2 * q2] = v.x;
+          x[2 * q2 + 1] = v.y;
         }
-        id = bi;
-        nd = bd;
+        double nd;
+        if (fl) {  // ascending, strict <, sqrt domain (distance.py:106-116)
+          double bd = CUDART_INF;
+          int bi = 0;
+          for (int j = 0; j < k; ++j) {
+            const double dj = sqrt(exact_sq<DP>(x, crow + j * DP, d));
+            if (dj < bd) { bd = dj; bi = j; }
+          }
+          id = bi;
+          nd = bd;
+        } else {
+          nd = sqrt(exact_sq<DP>(x, crow + id * DP, d));
+        }
+        nd2 = nd * nd;
+        if (a.mti_seed && valid) {
+          a.upper[row0 + my_r] = nd;
+          a.tight[row0 + my_r] = 1;
+          my_sq = exact_sq<DP>(x, Zero{}, d);
+        }
       } else {
-        nd = sqrt(exact_sq<DP>(x, crow + id * DP, d));
+        // certified winner: dense WCSS from the norm form, ||x||^2 - 2 s (rounding ~1e-16 ||x||^2)
+        nd2 = fmax(xs - 2.0 * sb, 0.0);
       }
       my_id = id;
       if (valid) {
@@ -320,63 +357,83 @@ __global__ void __launch_bounds__(KNB_NT, 1)
         const int old = a.assign[row];
         a.assign[row] = id;
         reassigned += (old != id);
-        if (a.mti_seed) {
-          a.upper[row] = nd;
-          a.tight[row] = 1;
-          xsq[my_r] = exact_sq<DP>(x, Zero{}, d);
-        } else {
-          wcss += nd * nd;
-        }
+        if (!a.mti_seed) wcss += nd2;
         ++rows_done;
       }
     } else if (valid) {
       my_id = a.assign[row0 + my_r];
       ++rows_done;
     }
-    // ---- member masks in natural row order: bit p <-> row warp*32 + p
+
+    // ---- warp-local accumulation: sort rows by (cluster, row), then segment sums
     {
-      const int src = ((lane & 7) << 2) | (lane >> 3);  // lane owning row offset `lane`
-      const int idn = __shfl_sync(0xffffffffu, valid ? my_id : -1, src);
-      const unsigned peers = __match_any_sync(0xffffffffu, idn);
-      if (idn >= 0 && lane == __ffs(peers) - 1) masks[warp * k + idn] = peers;
-    }
-    __syncthreads();
-    {  // deterministic segmented accumulation, members in row order
-      constexpr int NG = KNB_NT / DP;
-      const int e = tid % DP, gg = tid / DP;
-      if (e < d) {
-        for (int j = gg; j < k; j += NG) {
-          double s = 0.0, cc = 0.0, q = 0.0;
+      const unsigned key = warp_sort(valid ? ((unsigned)my_id << 5) | (unsigned)my_r : 0xffffffffu, lane);
+      const bool kv = key != 0xffffffffu;
+      const int kid = (int)(key >> 5);
+      const int pid = __shfl_up_sync(0xffffffffu, kid, 1);
+      const int nid = __shfl_down_sync(0xffffffffu, kid, 1);
+      const bool nv = __shfl_down_sync(0xffffffffu, (int)kv, 1) != 0;
+      const bool st = kv && (lane == 0 || pid != kid);
+      const bool en = kv && (lane == 31 || !nv || nid != kid);
+      const unsigned smask = __ballot_sync(0xffffffffu, st);
+      const unsigned emask = __ballot_sync(0xffffffffu, en);
+      const int nvalid = __popc(__ballot_sync(0xffffffffu, kv));
+      // counts and squared norms: segmented inclusive scan over lanes (= sorted positions)
+      const int rr = (int)(key & 31);
+      double q = __shfl_sync(0xffffffffu, my_sq, ((rr & 7) << 2) | (rr >> 3));
+      const int head = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));  // segment start at or below lane
 #pragma unroll
-          for (int rg = 0; rg < RG; ++rg) {
-            unsigned m = masks[rg * k + j];
-            if (e == 0) cc += __popc(m);
-            while (m) {
-              const int l = __ffs(m) - 1;
-              m &= m - 1;
-              const int r = rg * 32 + l;
-              s += *reinterpret_cast<const double*>(tb + TL::elem_off(r, e, MR));
-              if (e == 0 && a.mti_seed) q += xsq[r];
-            }
+      for (int off = 1; off < 32; off <<= 1) {
+        const double up = __shfl_up_sync(0xffffffffu, q, off);
+        if (lane - off >= head) q += up;
+      }
+      if (en) {
+        cnt[kid] += (double)(lane - head + 1);
+        sqa[kid] += q;
+      }
+      // dims: lanes = dims; walk the sorted positions with a branch-free segmented sum
+      const int e0 = lane < d ? lane : 0;
+      const int e1 = lane + 32 < d ? lane + 32 : 0;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int p = 0; p < 32; ++p) {
+        if (p < nvalid) {
+          const unsigned kk = __shfl_sync(0xffffffffu, key, p);
+          const int r = (int)(kk & 31);
+          const double keep = ((smask >> p) & 1u) ? 0.0 : 1.0;
+          s0 = fma(s0, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e0, BR)));
+          if constexpr (DP > 32) s1 = fma(s1, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e1, BR)));
+          if ((emask >> p) & 1u) {
+            const int j = (int)(kk >> 5);
+            if (lane < d) acc[j * d + lane] += s0;
+            if constexpr (DP > 32) if (lane + 32 < d) acc[j * d + lane + 32] += s1;
           }
-          acc[j * DP + e] += s;
-          if (e == 0) { cnt[j] += cc; sqa[j] += q; }
         }
       }
     }
-    __syncthreads();  // tile buffer and masks free for reuse
-    buf ^= 1;
+    // ---- refill this stage with the block NS strides ahead
+    __syncwarp();
+    const long long nb = blk + (long long)NS * TW;
+    if (nb < nblk) {
+      fence_proxy_async();
+      load_block<DP>(&tmap, &bar[s], tb, nb, a, tma, lane);
+    }
   }
+  __syncthreads();
 
+  // CTA partial: warps' private sums added in warp order
   const long long Lg = acc_len(k, d);
   double* out = a.partials + (long long)blockIdx.x * Lg;
-  for (int i = tid; i < k * d; i += KNB_NT) {
-    const int j = i / d, e = i - j * d;
-    out[i] = acc[j * DP + e];
-  }
-  for (int j = tid; j < k; j += KNB_NT) {
-    out[(long long)k * d + j] = cnt[j];
-    out[(long long)k * d + k + j] = sqa[j];
+  const long long kd = (long long)k * d;
+  for (long long i = tid; i < kd + 2LL * k; i += blockDim.x) {
+    size_t off;
+    long long ii;
+    if (i < kd) { off = L.acc_off; ii = i; }
+    else if (i < kd + k) { off = L.cnt_off; ii = i - kd; }
+    else { off = L.sq_off; ii = i - kd - k; }
+    double v = 0.0;
+    for (int w = 0; w < W; ++w) v += reinterpret_cast<const double*>(smem + L.warp0 + (size_t)w * L.per_warp + off)[ii];
+    out[i] = v;
   }
   const double r_re = (double)warp_sum_ll(reassigned);
   const double r_w = warp_sum(wcss);
@@ -385,8 +442,8 @@ __global__ void __launch_bounds__(KNB_NT, 1)
   __syncthreads();
   if (tid == 0) {
     double t_re = 0, t_w = 0, t_rows = 0;
-    for (int w = 0; w < KNB_WARPS; ++w) { t_re += red[w * 4]; t_w += red[w * 4 + 1]; t_rows += red[w * 4 + 2]; }
-    double* sc = out + (long long)k * d + 2LL * k;
+    for (int w = 0; w < W; ++w) { t_re += red[w * 4]; t_w += red[w * 4 + 1]; t_rows += red[w * 4 + 2]; }
+    double* sc = out + kd + 2LL * k;
     for (int i = 0; i < NSCAL; ++i) sc[i] = 0.0;
     sc[S_REASSIGNED] = t_re;
     sc[S_WCSS] = t_w;
@@ -395,12 +452,22 @@ __global__ void __launch_bounds__(KNB_NT, 1)
   }
 }
 
+constexpr size_t SMEM_MAX = 227 * 1024;
+
+int warps_for(int DP, int k, int d) {
+  for (int W = KNB_WARPS; W >= 1; W >>= 1)
+    if (WarpSmem(DP, k, d, W).total <= SMEM_MAX) return W;
+  return 0;
+}
+
 template <int DP>
 cudaError_t launch_mma_dp(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
-  const MmaSmem L(DP, a.k);
+  const int W = warps_for(DP, a.k, a.d);
+  if (!W) return cudaErrorInvalidValue;
+  const WarpSmem L(DP, a.k, a.d, W);
   cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  dense_mma_kernel<DP><<<grid, KNB_NT, L.total, s>>>(*tmap, a);
+  dense_mma_kernel<DP><<<grid, W * 32, L.total, s>>>(*tmap, a);
   return cudaGetLastError();
 }
 
@@ -415,9 +482,13 @@ int dense_mma_dp(int d) {
   return 0;
 }
 
-size_t dense_mma_smem(int DP, int k) { return MmaSmem(DP, k).total; }
+// 0 when even one warp's buffers do not fit (the generic kernel takes over)
+size_t dense_mma_smem(int DP, int k, int d) {
+  const int W = warps_for(DP, k, d);
+  return W ? WarpSmem(DP, k, d, W).total : (size_t)-1;
+}
 
-int dense_mma_rows() { return MR; }
+int dense_mma_rows() { return BR; }
 
 cudaError_t launch_dense_mma(const CUtensorMap* tmap, const DenseArgs& a, int DP, int grid, cudaStream_t s) {
   switch (DP) {

@@ -300,7 +300,7 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   }
   // kernel selection
   c->DP = dense_tile_dp(d);
-  if (c->DP && dense_tile_smem(c->DP, k) > SMEM_LIMIT) c->DP = 0;
+  if (c->DP && dense_tile_smem(c->DP, k, d) > SMEM_LIMIT) c->DP = 0;
   c->DPm = dense_tile_dp(d);
   c->half_in_smem = 0;
   if (c->DPm) {
@@ -311,7 +311,7 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   {
     const long long rows = dense_rows_per_tile(c->DP);
     const long long tiles = (nl + rows - 1) / rows;
-    long long g = c->DP ? dense_tile_grid(c->DP, k, c->sms) : 4LL * c->sms;
+    long long g = c->DP ? dense_tile_grid(c->DP, k, d, c->sms) : 4LL * c->sms;
     c->G_dense = (int)(tiles < g ? tiles : g);
   }
   {

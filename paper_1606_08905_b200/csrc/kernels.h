@@ -62,16 +62,16 @@ struct FinalArgs {
 
 // kernel selection helpers
 int dense_mma_dp(int d);
-size_t dense_mma_smem(int DP, int k);
+size_t dense_mma_smem(int DP, int k, int d);
 int dense_mma_rows();
 cudaError_t launch_dense_mma(const CUtensorMap* tmap, const DenseArgs& a, int DP, int grid, cudaStream_t s);
 int dense_tile_dp(int d);                       // padded dim for the register path, 0 = generic
-size_t dense_tile_smem(int DP, int k);
+size_t dense_tile_smem(int DP, int k, int d);
 size_t mti_tile_smem(int DP, int k, int half_in_smem);
 
 cudaError_t launch_dense(const CUtensorMap* tmap, const DenseArgs& a, int DP, int grid, cudaStream_t s);
 cudaError_t launch_mti(const MtiArgs& a, int DP, int grid, cudaStream_t s);
-int dense_tile_grid(int DP, int k, int sms);     // CTAs per device for the register path
+int dense_tile_grid(int DP, int k, int d, int sms);  // CTAs per device for the tensor-core path
 int mti_tile_grid(int DP, int k, int half_in_smem, int sms);
 int dense_rows_per_tile(int DP);
 
