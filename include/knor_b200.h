@@ -125,9 +125,21 @@ int knb_get_bounds(knb_ctx* ctx, double* upper, uint8_t* tight);
 int knb_sync(knb_ctx* ctx);
 /* Benchmark hook: keep running full iterations after convergence (kmeans() never sets it). */
 int knb_set_ignore_stop(knb_ctx* ctx, int32_t on);
+/* Options.  KNB_OPT_MTI_SCAN selects how a pruned iteration re-assigns the survivors of the
+ * point-skip test (clause 1): KNB_MTI_EXACT walks the candidates with clauses 2/3 exactly like
+ * scan_block (pruning.py:163-204), reproducing its dist_comps / pruned_* counters;
+ * KNB_MTI_DENSE scores survivors on the FP64 tensor cores (certified argmin, exact bound) --
+ * identical assignments, bounds, skips and centroids, dist_comps = k per survivor;
+ * KNB_MTI_AUTO (default) = DENSE where available (d <= 64, centroids fit shared memory). */
+#define KNB_OPT_MTI_SCAN 1
+#define KNB_MTI_AUTO 0
+#define KNB_MTI_EXACT 1
+#define KNB_MTI_DENSE 2
+int knb_set_option(knb_ctx* ctx, int32_t option, int64_t value);
 /* Device bytes held by the context (the GPU analogue of KmeansResult.peak_state_bytes). */
 int knb_state_bytes(knb_ctx* ctx, int64_t* bytes);
-/* Which kernels the context uses: padded width (0 = generic), TMA on/off, grid sizes. */
+/* Which kernels the context uses: padded width (0 = generic), TMA on/off, grid sizes
+ * (grid_mti < 0: the tensor-core MTI kernel with -grid_mti CTAs). */
 int knb_describe(knb_ctx* ctx, int32_t* dense_dp, int32_t* use_tma, int32_t* grid_dense, int32_t* grid_mti);
 
 /* Roofline denominators measured on the device: FP64 FMA rate (DFMA/s, 8 independent chains

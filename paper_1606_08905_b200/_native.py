@@ -17,6 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libknorb200.so")
 
 KNB_E_ARG, KNB_E_CUDA, KNB_E_STATE, KNB_E_COUNT, KNB_E_NOMEM = -1, -2, -3, -4, -5
+KNB_OPT_MTI_SCAN = 1
+MTI_SCAN = {"auto": 0, "exact": 1, "dense": 2}
 
 
 class NativeUnavailable(RuntimeError):
@@ -81,6 +83,7 @@ SIGNATURES = {
     "knb_state_bytes": [_P, _PI64],
     "knb_describe": [_P, _PI32, _PI32, _PI32, _PI32],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
+    "knb_set_option": [_P, _I32, _I64],
 }
 
 _lib = None
@@ -285,6 +288,9 @@ class Context:
     def set_ignore_stop(self, on: bool) -> None:
         check(self.L.knb_set_ignore_stop(self.h, int(on)))
 
+    def set_option(self, option: int, value: int) -> None:
+        check(self.L.knb_set_option(self.h, option, value))
+
     def state_bytes(self) -> int:
         v = ctypes.c_int64()
         check(self.L.knb_state_bytes(self.h, ctypes.byref(v)))
@@ -293,7 +299,8 @@ class Context:
     def describe(self) -> dict:
         a, b, c, d = (ctypes.c_int32() for _ in range(4))
         check(self.L.knb_describe(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
-        return dict(dense_dp=a.value, tma=bool(b.value), grid_dense=c.value, grid_mti=d.value)
+        return dict(dense_dp=a.value, tma=bool(b.value), grid_dense=c.value,
+                    grid_mti=abs(d.value), mti_kernel="tensor-core" if d.value < 0 else "exact-scan")
 
 
 def device_info(device: int = 0) -> dict:

@@ -38,12 +38,13 @@ __global__ void __launch_bounds__(KNB_NT) dense_generic_kernel(const DenseArgs a
     for (int i = tid; i < KNB_WARPS * k; i += KNB_NT) masks[i] = 0u;
     const long long row = tile * KNB_NT + tid;
     const bool valid = row < a.n;
-    int bid = -1;
+    int bid = -1, oldid = -1;
     if (valid) {
       const double* x = a.X + row * d;
       if (labels) {
         bid = a.assign[row];
       } else {
+        oldid = a.assign[row];
         double bd = CUDART_INF, lo = CUDART_INF, hi = CUDART_INF;
         int bi = 0;
         for (int j = 0; j < k; ++j) {
@@ -72,31 +73,40 @@ __global__ void __launch_bounds__(KNB_NT) dense_generic_kernel(const DenseArgs a
       }
       ++rows_done;
     }
-    __syncthreads();
-    {
-      const unsigned peers = __match_any_sync(0xffffffffu, bid);
-      if (bid >= 0 && lane == __ffs(peers) - 1) masks[warp * k + bid] = peers;
-    }
-    __syncthreads();
     const long long row0 = tile * KNB_NT;
-    for (long long pi = tid; pi < (long long)k * d; pi += KNB_NT) {
-      const int j = (int)(pi / d), e = (int)(pi - (long long)j * d);
-      double s = 0.0, c = 0.0, q = 0.0;
-      for (int w = 0; w < KNB_WARPS; ++w) {
-        unsigned m = masks[w * k + j];
-        if (e == 0) c += __popc(m);
-        while (m) {
-          const int l = __ffs(m) - 1;
-          m &= m - 1;
-          const int r = w * 32 + l;
-          s += a.X[(row0 + r) * d + e];
-          if (e == 0 && a.mti_seed) q += xsq[r];
-        }
+    // full passes add every row; later dense passes add moved rows to their new
+    // cluster (sign +1) and remove them from the old one (sign -1)
+    const bool moved = valid && !labels && bid != oldid;
+    for (int pass = 0; pass < (a.delta ? 2 : 1); ++pass) {
+      const double sign = pass ? -1.0 : 1.0;
+      const int accid = !a.delta ? bid : (moved ? (pass ? oldid : bid) : -1);
+      __syncthreads();
+      if (pass) for (int i = tid; i < KNB_WARPS * k; i += KNB_NT) masks[i] = 0u;
+      __syncthreads();
+      {
+        const unsigned peers = __match_any_sync(0xffffffffu, accid);
+        if (accid >= 0 && lane == __ffs(peers) - 1) masks[warp * k + accid] = peers;
       }
-      out[pi] += s;
-      if (e == 0) {
-        out[(long long)k * d + j] += c;
-        out[(long long)k * d + k + j] += q;
+      __syncthreads();
+      for (long long pi = tid; pi < (long long)k * d; pi += KNB_NT) {
+        const int j = (int)(pi / d), e = (int)(pi - (long long)j * d);
+        double s = 0.0, c = 0.0, q = 0.0;
+        for (int w = 0; w < KNB_WARPS; ++w) {
+          unsigned m = masks[w * k + j];
+          if (e == 0) c += __popc(m);
+          while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int r = w * 32 + l;
+            s += a.X[(row0 + r) * d + e];
+            if (e == 0 && a.mti_seed) q += xsq[r];
+          }
+        }
+        out[pi] += sign * s;
+        if (e == 0) {
+          out[(long long)k * d + j] += sign * c;
+          out[(long long)k * d + k + j] += sign * q;
+        }
       }
     }
     __syncthreads();

@@ -40,12 +40,11 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "mma_common.cuh"
 
 namespace knb {
 
 namespace {
-
-constexpr int BR = 32;  // rows per warp block
 
 __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -75,52 +74,6 @@ struct WarpSmem {
     total = warp0 + (size_t)W * per_warp;
   }
 };
-
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void score_update(double& best, int& bid, bool& flag, double s, int j, int tolhi) {
-  const double diff = __dsub_rn(s, best);
-  const int h = __double2hiint(diff);
-  const bool better = h > 0;
-  const bool near = (h & 0x7fffffff) <= tolhi;
-  flag = near | (flag & !better);
-  best = better ? s : best;
-  bid = better ? j : bid;
-}
-
-// merge a disjoint partial (best, id, flag) held by lane ^ lanemask
-__device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int tolhi, int lanemask) {
-  const double ob = __shfl_xor_sync(0xffffffffu, best, lanemask);
-  const int oi = __shfl_xor_sync(0xffffffffu, bid, lanemask);
-  const bool of = __shfl_xor_sync(0xffffffffu, (int)flag, lanemask) != 0;
-  const double diff = __dsub_rn(ob, best);
-  const int h = __double2hiint(diff);
-  const bool near = (h & 0x7fffffff) <= tolhi;
-  const bool other = h > 0 || (diff == 0.0 && oi < bid);
-  flag = near | (other ? of : flag);
-  best = other ? ob : best;
-  bid = other ? oi : bid;
-}
-
-// ascending bitonic sort of one 32-bit key per lane
-__device__ __forceinline__ unsigned warp_sort(unsigned key, int lane) {
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const unsigned other = __shfl_xor_sync(0xffffffffu, key, stride);
-      const bool up = size == 32 ? true : ((lane & size) == 0);
-      const bool lower = (lane & stride) == 0;
-      const unsigned lo = key < other ? key : other, hi = key < other ? other : key;
-      key = (lower == up) ? lo : hi;
-    }
-  }
-  return key;
-}
 
 template <int DP>
 __device__ __forceinline__ void load_block(const CUtensorMap* tmap, uint64_t* bar, unsigned char* dst, long long blk,
@@ -158,7 +111,6 @@ __global__ void __launch_bounds__(KNB_NT, 1)
     dense_mma_kernel(const __grid_constant__ CUtensorMap tmap, const DenseArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;         // k-steps of 4 dims
-  constexpr bool ACACHE = DP <= 32;  // point fragments stay in registers across centroid blocks
   constexpr int NS = DP <= 8 ? 4 : 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -237,179 +189,48 @@ __global__ void __launch_bounds__(KNB_NT, 1)
     const long long row0 = blk * BR;
     const int my_r = t4 * 8 + g;  // the row this lane finishes after the quad combine
     const bool valid = row0 + my_r < a.n;
-    int my_id = 0;
+    const long long row = row0 + my_r;
+    int id = 0, old = -1;
     double my_sq = 0.0;
-
+    if (valid) old = a.assign[row];
     if (!labels) {
-      // ---- point fragments: A[m][kk] = x[pg*8 + g][s*4 + t4]
-      double afr[4][ACACHE ? KS : 1];
-      double xn2[4];
-#pragma unroll
-      for (int pg = 0; pg < 4; ++pg) {
-        double s2 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const double v = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
-          if constexpr (ACACHE) afr[pg][ks] = v;
-          s2 = fma(v, v, s2);
-        }
-        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
-        xn2[pg] = s2;
-      }
-      double best[4];
-      int bid[4], tolhi[4];
-      bool flag[4];
-#pragma unroll
-      for (int pg = 0; pg < 4; ++pg) {
-        tolhi[pg] = __double2hiint(tolk * (xn2[pg] + cmax2));
-        best[pg] = -CUDART_INF;
-        bid[pg] = 0;
-        flag[pg] = false;
-      }
-#pragma unroll 1
-      for (int cb = 0; cb < ntile8; cb += 4) {
-        const int nq = ntile8 - cb < 4 ? ntile8 - cb : 4;
-        double c[4][4][2];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 h = q < nq ? *reinterpret_cast<const double2*>(chn + (cb + q) * 8 + 2 * t4)
-                                   : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int pg = 0; pg < 4; ++pg) { c[pg][q][0] = h.x; c[pg][q][1] = h.y; }
-        }
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          double av[4];
-#pragma unroll
-          for (int pg = 0; pg < 4; ++pg) {
-            if constexpr (ACACHE) av[pg] = afr[pg][ks];
-            else av[pg] = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q < nq) {
-              const double bv = bf[(((cb + q) * KS + ks) << 5) + lane];
-#pragma unroll
-              for (int pg = 0; pg < 4; ++pg) dmma(c[pg][q], av[pg], bv);
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q < nq) {
-            const int j0 = (cb + q) * 8 + 2 * t4;
-#pragma unroll
-            for (int pg = 0; pg < 4; ++pg) {
-              score_update(best[pg], bid[pg], flag[pg], c[pg][q][0], j0, tolhi[pg]);
-              score_update(best[pg], bid[pg], flag[pg], c[pg][q][1], j0 + 1, tolhi[pg]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int pg = 0; pg < 4; ++pg) {
-        combine(best[pg], bid[pg], flag[pg], tolhi[pg], 1);
-        combine(best[pg], bid[pg], flag[pg], tolhi[pg], 2);
-      }
-      int id = bid[0];
-      bool fl = flag[0];
-      double sb = best[0], xs = xn2[0];
-#pragma unroll
-      for (int pg = 1; pg < 4; ++pg)
-        if (t4 == pg) { id = bid[pg]; fl = flag[pg]; sb = best[pg]; xs = xn2[pg]; }
-      double nd2 = 0.0;  // squared nearest distance
-      if (fl || a.mti_seed) {
-        // exact recipe on the lane's own row: near-tie re-rank, or the MTI bound seed
-        double x[DP];
-#pragma unroll
-        for (int q2 = 0; q2 < DP / 2; ++q2) {
-          const double2 v = *reinterpret_cast<const double2*>(tb + TL::chunk_off(my_r, q2, BR));
-          x[2 * q2] = v.x;
-          x[2 * q2 + 1] = v.y;
-        }
-        double nd;
-        if (fl) {  // ascending, strict <, sqrt domain (distance.py:106-116)
-          double bd = CUDART_INF;
-          int bi = 0;
-          for (int j = 0; j < k; ++j) {
-            const double dj = sqrt(exact_sq<DP>(x, crow + j * DP, d));
-            if (dj < bd) { bd = dj; bi = j; }
-          }
-          id = bi;
-          nd = bd;
-        } else {
-          nd = sqrt(exact_sq<DP>(x, crow + id * DP, d));
-        }
+      const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+      id = sc.id;
+      double nd2;
+      if (sc.flag || a.mti_seed) {
+        // exact recipe: near-tie re-rank, or the MTI bound seed (engine.py:305-308)
+        const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, id, a.mti_seed ? &my_sq : nullptr);
         nd2 = nd * nd;
         if (a.mti_seed && valid) {
-          a.upper[row0 + my_r] = nd;
-          a.tight[row0 + my_r] = 1;
-          my_sq = exact_sq<DP>(x, Zero{}, d);
+          a.upper[row] = nd;
+          a.tight[row] = 1;
         }
       } else {
-        // certified winner: dense WCSS from the norm form, ||x||^2 - 2 s (rounding ~1e-16 ||x||^2)
-        nd2 = fmax(xs - 2.0 * sb, 0.0);
+        // certified winner: WCSS term from the norm form ||x||^2 - 2 s (rounding ~1e-16 ||x||^2)
+        nd2 = fmax(sc.xn2 - 2.0 * sc.best, 0.0);
       }
-      my_id = id;
       if (valid) {
-        const long long row = row0 + my_r;
-        const int old = a.assign[row];
-        a.assign[row] = id;
-        reassigned += (old != id);
+        if (id != old) {
+          a.assign[row] = id;
+          ++reassigned;
+        }
         if (!a.mti_seed) wcss += nd2;
         ++rows_done;
       }
     } else if (valid) {
-      my_id = a.assign[row0 + my_r];
+      id = old;
       ++rows_done;
     }
-
-    // ---- warp-local accumulation: sort rows by (cluster, row), then segment sums
-    {
-      const unsigned key = warp_sort(valid ? ((unsigned)my_id << 5) | (unsigned)my_r : 0xffffffffu, lane);
-      const bool kv = key != 0xffffffffu;
-      const int kid = (int)(key >> 5);
-      const int pid = __shfl_up_sync(0xffffffffu, kid, 1);
-      const int nid = __shfl_down_sync(0xffffffffu, kid, 1);
-      const bool nv = __shfl_down_sync(0xffffffffu, (int)kv, 1) != 0;
-      const bool st = kv && (lane == 0 || pid != kid);
-      const bool en = kv && (lane == 31 || !nv || nid != kid);
-      const unsigned smask = __ballot_sync(0xffffffffu, st);
-      const unsigned emask = __ballot_sync(0xffffffffu, en);
-      const int nvalid = __popc(__ballot_sync(0xffffffffu, kv));
-      // counts and squared norms: segmented inclusive scan over lanes (= sorted positions)
-      const int rr = (int)(key & 31);
-      double q = __shfl_sync(0xffffffffu, my_sq, ((rr & 7) << 2) | (rr >> 3));
-      const int head = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));  // segment start at or below lane
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const double up = __shfl_up_sync(0xffffffffu, q, off);
-        if (lane - off >= head) q += up;
-      }
-      if (en) {
-        cnt[kid] += (double)(lane - head + 1);
-        sqa[kid] += q;
-      }
-      // dims: lanes = dims; walk the sorted positions with a branch-free segmented sum
-      const int e0 = lane < d ? lane : 0;
-      const int e1 = lane + 32 < d ? lane + 32 : 0;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int p = 0; p < 32; ++p) {
-        if (p < nvalid) {
-          const unsigned kk = __shfl_sync(0xffffffffu, key, p);
-          const int r = (int)(kk & 31);
-          const double keep = ((smask >> p) & 1u) ? 0.0 : 1.0;
-          s0 = fma(s0, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e0, BR)));
-          if constexpr (DP > 32) s1 = fma(s1, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e1, BR)));
-          if ((emask >> p) & 1u) {
-            const int j = (int)(kk >> 5);
-            if (lane < d) acc[j * d + lane] += s0;
-            if constexpr (DP > 32) if (lane + 32 < d) acc[j * d + lane + 32] += s1;
-          }
-        }
-      }
+    if (!a.delta) {
+      accumulate_rows<DP>(valid ? ((unsigned)id << 5) | (unsigned)my_r : 0xffffffffu, my_sq, 1.0, tb, acc, cnt,
+                          sqa, d, lane);
+    } else {
+      // steady-state dense passes: running sums move by the reassigned rows only
+      const bool moved = valid && id != old;
+      accumulate_rows<DP>(moved ? ((unsigned)id << 5) | (unsigned)my_r : 0xffffffffu, 0.0, 1.0, tb, acc, cnt, sqa,
+                          d, lane);
+      accumulate_rows<DP>(moved ? ((unsigned)old << 5) | (unsigned)my_r : 0xffffffffu, 0.0, -1.0, tb, acc, cnt,
+                          sqa, d, lane);
     }
     // ---- refill this stage with the block NS strides ahead
     __syncwarp();

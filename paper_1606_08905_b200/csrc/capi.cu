@@ -53,7 +53,9 @@ struct knb_ctx {
   int use_tma = 0;
 
   int DP = 0, DPm = 0, half_in_smem = 0;
-  int G_dense = 1, G_mti = 1;
+  int G_dense = 1, G_mti = 1, G_mti_mma = 1;
+  int mti_scan = 0;   // KNB_MTI_AUTO / KNB_MTI_EXACT / KNB_MTI_DENSE
+  bool mti_mma_ok = false;
 
   int32_t* assign = nullptr;
   double* upper = nullptr;
@@ -126,7 +128,7 @@ int reset_run(knb_ctx* c) {
   h.tolerance = c->tolerance;
   KNB_CUDA(cudaMemcpyAsync(c->ctrl, &h, offsetof(Ctrl, cmax2), cudaMemcpyHostToDevice, c->stream));
   KNB_CUDA(cudaMemsetAsync(c->assign, 0, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
-  if (c->pruning) KNB_CUDA(cudaMemsetAsync(c->run, 0, sizeof(double) * c->L, c->stream));
+  KNB_CUDA(cudaMemsetAsync(c->run, 0, sizeof(double) * c->L, c->stream));
   c->t_host = 0;
   return KNB_OK;
 }
@@ -184,6 +186,7 @@ int launch_local(knb_ctx* c) {
     a.tight = c->tight;
     a.mti_seed = c->pruning;
     a.labels_only = 0;
+    a.delta = (!c->pruning && c->t_host > 0) ? 1 : 0;
     a.means = c->means;
     a.chn = c->chn;
     a.partials = c->partials;
@@ -204,11 +207,17 @@ int launch_local(knb_ctx* c) {
     a.drift = c->drift;
     a.half = c->half;
     a.half_min = c->half_min;
+    a.chn = c->chn;
     a.partials = c->partials;
     a.ctrl = c->ctrl;
     a.half_in_smem = c->half_in_smem;
-    KNB_CUDA(launch_mti(a, c->DPm, c->G_mti, c->stream));
-    KNB_CUDA(launch_reduce(c->partials, c->G_mti, c->L, c->exch, c->ctrl, c->stream));
+    if (c->mti_scan != KNB_MTI_EXACT && c->mti_mma_ok) {
+      KNB_CUDA(launch_mti_mma(a, c->DP, c->G_mti_mma, c->stream));
+      KNB_CUDA(launch_reduce(c->partials, c->G_mti_mma, c->L, c->exch, c->ctrl, c->stream));
+    } else {
+      KNB_CUDA(launch_mti(a, c->DPm, c->G_mti, c->stream));
+      KNB_CUDA(launch_reduce(c->partials, c->G_mti, c->L, c->exch, c->ctrl, c->stream));
+    }
   }
   return KNB_OK;
 }
@@ -320,18 +329,24 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     long long g = c->DPm ? mti_tile_grid(c->DPm, k, c->half_in_smem, c->sms) : 4LL * c->sms;
     c->G_mti = (int)(tiles < g ? tiles : g);
   }
+  c->mti_mma_ok = c->DP != 0 && mti_mma_fits(c->DP, k, d);
+  {
+    const long long tiles = (nl + 31) / 32;
+    c->G_mti_mma = (int)(tiles < c->sms ? tiles : c->sms);
+  }
   c->L = acc_len(k, d);
   c->G_alloc = c->G_dense > c->G_mti ? c->G_dense : c->G_mti;
+  if (c->G_mti_mma > c->G_alloc) c->G_alloc = c->G_mti_mma;
   const size_t kd = (size_t)k * d;
   if ((rc = dev_alloc(c, &c->assign, nl))) return bail(rc);
   if (c->pruning) {
     if ((rc = dev_alloc(c, &c->upper, nl))) return bail(rc);
     if ((rc = dev_alloc(c, &c->tight, nl))) return bail(rc);
-    if ((rc = dev_alloc(c, &c->run, c->L))) return bail(rc);
     if ((rc = dev_alloc(c, &c->half, (size_t)k * k))) return bail(rc);
     if ((rc = dev_alloc(c, &c->half_min, k))) return bail(rc);
     if (cudaMemsetAsync(c->tight, 0, nl, c->stream) != cudaSuccess) return bail(fail(KNB_E_CUDA, "memset"));
   }
+  if ((rc = dev_alloc(c, &c->run, c->L))) return bail(rc);
   if ((rc = dev_alloc(c, &c->means, kd))) return bail(rc);
   if ((rc = dev_alloc(c, &c->prev, kd))) return bail(rc);
   if ((rc = dev_alloc(c, &c->stage, kd))) return bail(rc);
@@ -490,6 +505,7 @@ int knb_init_partition_local(knb_ctx* c, const int32_t* labels) {
   a.tight = c->tight;
   a.mti_seed = 0;
   a.labels_only = 1;
+  a.delta = 0;
   a.means = c->means;
   a.chn = c->chn;
   a.partials = c->partials;
@@ -728,6 +744,18 @@ int knb_set_ignore_stop(knb_ctx* c, int32_t on) {
   return KNB_OK;
 }
 
+int knb_set_option(knb_ctx* c, int32_t option, int64_t value) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (option == KNB_OPT_MTI_SCAN) {
+    if (value < KNB_MTI_AUTO || value > KNB_MTI_DENSE) return fail(KNB_E_ARG, "bad MTI scan mode");
+    if (value == KNB_MTI_DENSE && !c->mti_mma_ok)
+      return fail(KNB_E_ARG, "dense MTI scan needs d <= 64 and centroids that fit shared memory");
+    c->mti_scan = (int)value;
+    return KNB_OK;
+  }
+  return fail(KNB_E_ARG, "unknown option " + std::to_string(option));
+}
+
 int knb_state_bytes(knb_ctx* c, int64_t* bytes) {
   if (!c || !bytes) return fail(KNB_E_ARG, "null argument");
   *bytes = c->bytes;
@@ -739,7 +767,7 @@ int knb_describe(knb_ctx* c, int32_t* dp, int32_t* tma, int32_t* gd, int32_t* gm
   if (dp) *dp = c->DP;
   if (tma) *tma = c->use_tma;
   if (gd) *gd = c->G_dense;
-  if (gm) *gm = c->G_mti;
+  if (gm) *gm = (c->mti_scan != KNB_MTI_EXACT && c->mti_mma_ok) ? -c->G_mti_mma : c->G_mti;
   return KNB_OK;
 }
 

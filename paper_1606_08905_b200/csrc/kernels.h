@@ -18,6 +18,7 @@ struct DenseArgs {
   uint8_t* tight;
   int mti_seed;          // 1 on the full pass of a pruned run
   int labels_only;       // accumulate by the labels already in assign (random-partition init)
+  int delta;             // dense passes after the first: accumulate signed deltas of moved rows only
   const double* means;   // k x d
   const double* chn;     // k: -0.5 * ||c_j||^2
   double* partials;      // G x acc_len(k, d)
@@ -36,6 +37,7 @@ struct MtiArgs {
   const double* drift;
   const double* half;      // k x k
   const double* half_min;  // k
+  const double* chn;       // -0.5 ||c||^2 (tensor-core scan)
   double* partials;
   const Ctrl* ctrl;
   int half_in_smem;
@@ -71,6 +73,8 @@ size_t mti_tile_smem(int DP, int k, int half_in_smem);
 
 cudaError_t launch_dense(const CUtensorMap* tmap, const DenseArgs& a, int DP, int grid, cudaStream_t s);
 cudaError_t launch_mti(const MtiArgs& a, int DP, int grid, cudaStream_t s);
+bool mti_mma_fits(int DP, int k, int d);
+cudaError_t launch_mti_mma(const MtiArgs& a, int DP, int grid, cudaStream_t s);
 int dense_tile_grid(int DP, int k, int d, int sms);  // CTAs per device for the tensor-core path
 int mti_tile_grid(int DP, int k, int half_in_smem, int sms);
 int dense_rows_per_tile(int DP);

@@ -1,0 +1,243 @@
+// Warp-level building blocks shared by the tensor-core kernels (assign_mma.cu,
+// mti_mma.cu): DMMA scoring of a 32-row block against all centroids with the
+// near-tie certificate, and the deterministic warp-local segmented accumulation.
+#pragma once
+
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace knb {
+
+constexpr int BR = 32;  // rows per warp block
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// running argmax with the near-tie flag; integer ops on the high word of s - best
+__device__ __forceinline__ void score_update(double& best, int& bid, bool& flag, double s, int j, int tolhi) {
+  const double diff = __dsub_rn(s, best);
+  const int h = __double2hiint(diff);
+  const bool better = h > 0;
+  const bool near = (h & 0x7fffffff) <= tolhi;
+  flag = near | (flag & !better);
+  best = better ? s : best;
+  bid = better ? j : bid;
+}
+
+// merge the disjoint partial (best, id, flag) held by lane ^ lanemask
+__device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int tolhi, int lanemask) {
+  const double ob = __shfl_xor_sync(0xffffffffu, best, lanemask);
+  const int oi = __shfl_xor_sync(0xffffffffu, bid, lanemask);
+  const bool of = __shfl_xor_sync(0xffffffffu, (int)flag, lanemask) != 0;
+  const double diff = __dsub_rn(ob, best);
+  const int h = __double2hiint(diff);
+  const bool near = (h & 0x7fffffff) <= tolhi;
+  const bool other = h > 0 || (diff == 0.0 && oi < bid);
+  flag = near | (other ? of : flag);
+  best = other ? ob : best;
+  bid = other ? oi : bid;
+}
+
+// ascending bitonic sort of one 32-bit key per lane
+__device__ __forceinline__ unsigned warp_sort(unsigned key, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const unsigned other = __shfl_xor_sync(0xffffffffu, key, stride);
+      const bool up = size == 32 ? true : ((lane & size) == 0);
+      const bool lower = (lane & stride) == 0;
+      const unsigned lo = key < other ? key : other, hi = key < other ? other : key;
+      key = (lower == up) ? lo : hi;
+    }
+  }
+  return key;
+}
+
+// Lane that finishes row r of a block after the quad combine (row = t4*8 + g).
+__device__ __forceinline__ int owner_lane(int r) { return ((r & 7) << 2) | (r >> 3); }
+
+struct Scored {
+  int id;       // certified argmax (or 0 when uncertified)
+  bool flag;    // near tie: caller re-ranks with the exact recipe
+  double best;  // s of the winner (x.c - ||c||^2/2)
+  double xn2;   // ||x||^2 of the lane's row
+};
+
+// Score the 32 rows of a block (TileLayout<DP>, BR rows at tb) against every centroid.
+// bf: centroids in B-fragment order, chn: -||c||^2/2 (dummy columns -inf).
+// Each lane returns the result for its row owner_lane^-1(lane) = t4*8 + g.
+template <int DP>
+__device__ __forceinline__ Scored score_block(const unsigned char* tb, const double* bf, const double* chn,
+                                              int ntile8, double tolk, double cmax2, int lane) {
+  using TL = TileLayout<DP>;
+  constexpr int KS = DP / 4;
+  constexpr bool ACACHE = DP <= 32;
+  const int g = lane >> 2, t4 = lane & 3;
+  double afr[4][ACACHE ? KS : 1];
+  double xn2[4];
+#pragma unroll
+  for (int pg = 0; pg < 4; ++pg) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double v = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
+      if constexpr (ACACHE) afr[pg][ks] = v;
+      s2 = fma(v, v, s2);
+    }
+    s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+    xn2[pg] = s2;
+  }
+  double best[4];
+  int bid[4], tolhi[4];
+  bool flag[4];
+#pragma unroll
+  for (int pg = 0; pg < 4; ++pg) {
+    tolhi[pg] = __double2hiint(tolk * (xn2[pg] + cmax2));
+    best[pg] = -CUDART_INF;
+    bid[pg] = 0;
+    flag[pg] = false;
+  }
+#pragma unroll 1
+  for (int cb = 0; cb < ntile8; cb += 4) {
+    const int nq = ntile8 - cb < 4 ? ntile8 - cb : 4;
+    double c[4][4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 h = q < nq ? *reinterpret_cast<const double2*>(chn + (cb + q) * 8 + 2 * t4) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int pg = 0; pg < 4; ++pg) { c[pg][q][0] = h.x; c[pg][q][1] = h.y; }
+    }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double av[4];
+#pragma unroll
+      for (int pg = 0; pg < 4; ++pg) {
+        if constexpr (ACACHE) av[pg] = afr[pg][ks];
+        else av[pg] = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q < nq) {
+          const double bv = bf[(((cb + q) * KS + ks) << 5) + lane];
+#pragma unroll
+          for (int pg = 0; pg < 4; ++pg) dmma(c[pg][q], av[pg], bv);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < nq) {
+        const int j0 = (cb + q) * 8 + 2 * t4;
+#pragma unroll
+        for (int pg = 0; pg < 4; ++pg) {
+          score_update(best[pg], bid[pg], flag[pg], c[pg][q][0], j0, tolhi[pg]);
+          score_update(best[pg], bid[pg], flag[pg], c[pg][q][1], j0 + 1, tolhi[pg]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int pg = 0; pg < 4; ++pg) {
+    combine(best[pg], bid[pg], flag[pg], tolhi[pg], 1);
+    combine(best[pg], bid[pg], flag[pg], tolhi[pg], 2);
+  }
+  Scored r{bid[0], flag[0], best[0], xn2[0]};
+#pragma unroll
+  for (int pg = 1; pg < 4; ++pg)
+    if (t4 == pg) { r.id = bid[pg]; r.flag = flag[pg]; r.best = best[pg]; r.xn2 = xn2[pg]; }
+  return r;
+}
+
+// Exact recipe on the lane's row: re-rank over every centroid (ascending, strict <,
+// sqrt domain, distance.py:106-116) when flagged, else the distance to `id`.
+template <int DP>
+__device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, const double* crow, int k, int d,
+                                               bool flag, int& id, double* sq_out) {
+  using TL = TileLayout<DP>;
+  double x[DP];
+#pragma unroll
+  for (int q2 = 0; q2 < DP / 2; ++q2) {
+    const double2 v = *reinterpret_cast<const double2*>(tb + TL::chunk_off(r, q2, BR));
+    x[2 * q2] = v.x;
+    x[2 * q2 + 1] = v.y;
+  }
+  double nd;
+  if (flag) {
+    double bd = CUDART_INF;
+    int bi = 0;
+    for (int j = 0; j < k; ++j) {
+      const double dj = sqrt(exact_sq<DP>(x, crow + j * DP, d));
+      if (dj < bd) { bd = dj; bi = j; }
+    }
+    id = bi;
+    nd = bd;
+  } else {
+    nd = sqrt(exact_sq<DP>(x, crow + id * DP, d));
+  }
+  if (sq_out) *sq_out = exact_sq<DP>(x, Zero{}, d);
+  return nd;
+}
+
+// Deterministic warp-local accumulation of the block rows selected by `key`
+// (= (cluster << 5) | row for included rows, ~0 otherwise), lanes = dims:
+//   acc[c][e] += sign * sum of x[row][e] over the rows of cluster c, in row order,
+//   cnt[c] += sign * members, sqa[c] += sign * sum of sq (sq held by owner_lane(row)).
+template <int DP>
+__device__ __forceinline__ void accumulate_rows(unsigned key, double my_sq, double sign, const unsigned char* tb,
+                                                double* acc, double* cnt, double* sqa, int d, int lane) {
+  using TL = TileLayout<DP>;
+  const unsigned inc = __ballot_sync(0xffffffffu, key != 0xffffffffu);
+  if (inc == 0u) return;
+  key = warp_sort(key, lane);
+  const bool kv = key != 0xffffffffu;
+  const int kid = (int)(key >> 5);
+  const int pid = __shfl_up_sync(0xffffffffu, kid, 1);
+  const int nid = __shfl_down_sync(0xffffffffu, kid, 1);
+  const bool nv = __shfl_down_sync(0xffffffffu, (int)kv, 1) != 0;
+  const bool st = kv && (lane == 0 || pid != kid);
+  const bool en = kv && (lane == 31 || !nv || nid != kid);
+  const unsigned smask = __ballot_sync(0xffffffffu, st);
+  const unsigned emask = __ballot_sync(0xffffffffu, en);
+  const int nvalid = __popc(inc);
+  // counts and squared norms: segmented inclusive scan over the sorted positions
+  const int rr = (int)(key & 31);
+  double q = __shfl_sync(0xffffffffu, my_sq, owner_lane(rr));
+  const int head = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double up = __shfl_up_sync(0xffffffffu, q, off);
+    if (lane - off >= head) q += up;
+  }
+  if (en) {
+    cnt[kid] += sign * (double)(lane - head + 1);
+    sqa[kid] += sign * q;
+  }
+  // dims: branch-free segmented sum along the sorted rows
+  const int e0 = lane < d ? lane : 0;
+  const int e1 = lane + 32 < d ? lane + 32 : 0;
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    if (p < nvalid) {
+      const unsigned kk = __shfl_sync(0xffffffffu, key, p);
+      const int r = (int)(kk & 31);
+      const double keep = ((smask >> p) & 1u) ? 0.0 : 1.0;
+      s0 = fma(s0, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e0, BR)));
+      if constexpr (DP > 32) s1 = fma(s1, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e1, BR)));
+      if ((emask >> p) & 1u) {
+        const int j = (int)(kk >> 5);
+        if (lane < d) acc[j * d + lane] += sign * s0;
+        if constexpr (DP > 32)
+          if (lane + 32 < d) acc[j * d + lane + 32] += sign * s1;
+      }
+    }
+  }
+}
+
+}  // namespace knb

@@ -1,0 +1,280 @@
+// K6 + K7 on the FP64 tensor cores: the pruned (MTI) iteration with survivors of
+// the point-skip test re-assigned by certified DMMA scoring.
+//
+// Replaces numakmeans engine._task_pruned (engine.py:321-354) + inflate_bounds
+// (pruning.py:152-160) + scan_block (pruning.py:163-204) with these semantics:
+//   prologue  u += drift[a]; tight &= (drift[a] == 0)        (bound inflation, fused)
+//   clause 1  the point is skipped when u <= half_min[a]      (inclusive; its row is never read)
+//   survivor  its new centroid is the exhaustive argmin (exactly what the reference's
+//             candidate scan returns -- pruning is sound and its distances are the exact
+//             recipe), its bound becomes the exact-recipe distance to that centroid and
+//             tight = 1, as in scan_block; moved points contribute signed deltas.
+// Assignments, bounds (and therefore every later skip decision), centroids and the
+// skip counts are the reference's; dist_comps counts the k distances evaluated per
+// survivor instead of the reference's clause-2/3 candidate walk (pruned_* are 0).  The
+// reference-counter walk stays available as the "exact" MTI scan (mti.cu).
+//
+// Layout: warp-independent.  A warp filters its strided 32-row blocks reading only the
+// 13 B/point state, appends survivors to a warp-private queue, and whenever 32 are
+// queued gathers their rows from HBM into a swizzled 32-row tile and scores them with
+// score_block (mma_common.cuh).  Deltas go through the warp-local sorted segment walk
+// into warp-private sums; the CTA adds its warps' sums in warp order.
+#include <cuda.h>
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "mma_common.cuh"
+
+namespace knb {
+
+namespace {
+
+__host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct MtiMmaSmem {
+  size_t bf, crow, chn, hmin, drift, red, warp0, tile_off, tile_stride, q_off, acc_off, cnt_off, sq_off, per_warp,
+      total;
+  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W) {
+    const int kp = (k + 7) & ~7;
+    size_t o = 0;
+    bf = o;    o += (size_t)kp * DP * 8;
+    crow = o;  o += (size_t)kp * DP * 8;
+    chn = o;   o += (size_t)kp * 8;
+    hmin = o;  o += (size_t)k * 8;
+    drift = o; o += (size_t)k * 8;
+    red = o;   o += 32 * 8 * 8;
+    o = al(o, 1024);
+    warp0 = o;
+    size_t w = 0;
+    tile_stride = (size_t)BR * DP * 8;
+    tile_off = w; w += 2 * tile_stride;  // two staging tiles (gather double buffer)
+    q_off = w;    w += 96 * 4 * 2;       // queued rows and their pre-scan assignment
+    acc_off = w;  w += (size_t)k * d * 8;
+    cnt_off = w;  w += (size_t)k * 8;
+    sq_off = w;   w += (size_t)k * 8;
+    per_warp = al(w, 1024);
+    total = warp0 + (size_t)W * per_warp;
+  }
+};
+
+template <int DP>
+__global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
+  using TL = TileLayout<DP>;
+  constexpr int KS = DP / 4;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
+  const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
+  const MtiMmaSmem L(DP, k, d, W);
+  double* bf = reinterpret_cast<double*>(smem + L.bf);
+  double* crow = reinterpret_cast<double*>(smem + L.crow);
+  double* chn = reinterpret_cast<double*>(smem + L.chn);
+  double* hmin = reinterpret_cast<double*>(smem + L.hmin);
+  double* drift = reinterpret_cast<double*>(smem + L.drift);
+  double* red = reinterpret_cast<double*>(smem + L.red);
+  unsigned char* wbase = smem + L.warp0 + (size_t)warp * L.per_warp;
+  unsigned char* tb = wbase + L.tile_off;
+  int* qrow = reinterpret_cast<int*>(wbase + L.q_off);
+  int* qorig = qrow + 96;
+  double* acc = reinterpret_cast<double*>(wbase + L.acc_off);
+  double* cnt = reinterpret_cast<double*>(wbase + L.cnt_off);
+  double* sqa = reinterpret_cast<double*>(wbase + L.sq_off);
+
+  for (int i = tid; i < kp * DP; i += blockDim.x) {
+    const int j = i / DP, e = i - j * DP;
+    crow[i] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
+    const int l = i & 31, qs = i >> 5, q = qs / KS, s = qs - q * KS;
+    const int jb = q * 8 + (l >> 2), eb = s * 4 + (l & 3);
+    bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
+  }
+  for (int j = tid; j < kp; j += blockDim.x) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
+  for (int j = tid; j < k; j += blockDim.x) {
+    hmin[j] = a.half_min[j];
+    drift[j] = a.drift[j];
+  }
+  for (int i = lane; i < k * d; i += 32) acc[i] = 0.0;
+  for (int j = lane; j < k; j += 32) { cnt[j] = 0.0; sqa[j] = 0.0; }
+  __syncthreads();
+
+  const double cmax2 = a.ctrl->cmax2;
+  const double tolk = (8.0 * d + 32.0) * 1.1102230246251565e-16;
+  const long long nblk = (a.n + BR - 1) / BR;
+  const long long gw = (long long)blockIdx.x * W + warp, TW = (long long)gridDim.x * W;
+  const bool vec = ((d & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
+  long long skips = 0, computed = 0, reassigned = 0;
+  int qn = 0;
+  // both staging tiles start zeroed: padded dims stay zero, rows past a batch hold stale finite data
+  for (int i = lane; i < 2 * BR * DP; i += 32) reinterpret_cast<double*>(tb)[i] = 0.0;
+  __syncwarp();
+
+  // async gather of queued entries [base, base + cnum) into a staging tile (rows 0..cnum-1)
+  auto gather = [&](unsigned char* dst, int base, int cnum) {
+    if (lane < cnum) {
+      const double* src = a.X + (long long)qrow[base + lane] * d;
+      if (vec) {
+#pragma unroll
+        for (int q2 = 0; q2 < DP / 2; ++q2)
+          if (2 * q2 < d) cp_async16(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
+      } else {
+#pragma unroll
+        for (int e = 0; e < DP; ++e)
+          if (e < d) cp_async8(dst + TL::elem_off(lane, e, BR), src + e);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // score and update the first `cnum` queued survivors (cnum <= 32), staged in tb
+  auto process = [&](const unsigned char* tb, int cnum) {
+    const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+    const int r = t4 * 8 + g;
+    const bool valid = r < cnum;
+    int id = sc.id;
+    double sq = 0.0;
+    const double nd = exact_winner<DP>(tb, r, crow, k, d, sc.flag, id, &sq);
+    const int orig = valid ? qorig[r] : 0;
+    const bool moved = valid && id != orig;
+    if (valid) {
+      const long long grow = qrow[r];
+      a.upper[grow] = nd;
+      a.tight[grow] = 1;
+      if (moved) {
+        a.assign[grow] = id;
+        ++reassigned;
+      }
+    }
+    if (lane == 0) computed += (long long)cnum * k;
+    accumulate_rows<DP>(moved ? ((unsigned)id << 5) | (unsigned)r : 0xffffffffu, sq, 1.0, tb, acc, cnt, sqa, d, lane);
+    accumulate_rows<DP>(moved ? ((unsigned)orig << 5) | (unsigned)r : 0xffffffffu, sq, -1.0, tb, acc, cnt, sqa, d,
+                        lane);
+    __syncwarp();
+  };
+
+  // filter strided blocks (bound inflation + clause 1) until `target` survivors are queued
+  long long blk = gw;
+  auto filter_until = [&](int target) {
+    while (qn < target && blk < nblk) {
+      const long long row = blk * BR + lane;
+      bool live = false;
+      int aa = 0;
+      if (row < a.n) {
+        aa = a.assign[row];
+        double u = a.upper[row];
+        const double dr = drift[aa];
+        if (dr != 0.0) {  // u + 0.0 == u and tight & true == tight: no store needed
+          u = u + dr;
+          a.upper[row] = u;
+          a.tight[row] = 0;
+        }
+        if (u <= hmin[aa]) ++skips;
+        else live = true;
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, live);
+      if (live) {
+        const int pos = qn + __popc(b & ((1u << lane) - 1u));
+        qrow[pos] = (int)row;
+        qorig[pos] = aa;
+      }
+      qn += __popc(b);
+      blk += TW;
+      __syncwarp();
+    }
+  };
+
+  // two staging tiles: the next batch's rows stream in while the current one is scored
+  int cur = 0;
+  filter_until(32);
+  int b0 = qn < 32 ? qn : 32;
+  if (b0 > 0) gather(tb, 0, b0);
+  while (b0 > 0) {
+    filter_until(64);
+    const int b1 = (b0 == 32 && qn > 32) ? (qn - 32 < 32 ? qn - 32 : 32) : 0;
+    unsigned char* tcur = tb + cur * L.tile_stride;
+    if (b1 > 0) {
+      gather(tb + (cur ^ 1) * L.tile_stride, 32, b1);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncwarp();
+    process(tcur, b0);
+    // pop the processed batch from the queue
+    const int rest = qn - b0;
+    for (int i0 = 0; i0 < rest; i0 += 32) {
+      int rr = 0, ro = 0;
+      if (i0 + lane < rest) { rr = qrow[b0 + i0 + lane]; ro = qorig[b0 + i0 + lane]; }
+      __syncwarp();
+      if (i0 + lane < rest) { qrow[i0 + lane] = rr; qorig[i0 + lane] = ro; }
+      __syncwarp();
+    }
+    qn = rest;
+    b0 = b1;
+    cur ^= 1;
+  }
+  __syncthreads();
+
+  const long long Lg = acc_len(k, d);
+  double* out = a.partials + (long long)blockIdx.x * Lg;
+  const long long kd = (long long)k * d;
+  for (long long i = tid; i < kd + 2LL * k; i += blockDim.x) {
+    size_t off;
+    long long ii;
+    if (i < kd) { off = L.acc_off; ii = i; }
+    else if (i < kd + k) { off = L.cnt_off; ii = i - kd; }
+    else { off = L.sq_off; ii = i - kd - k; }
+    double v = 0.0;
+    for (int w = 0; w < W; ++w) v += reinterpret_cast<const double*>(smem + L.warp0 + (size_t)w * L.per_warp + off)[ii];
+    out[i] = v;
+  }
+  const long long v0 = warp_sum_ll(reassigned), v1 = warp_sum_ll(computed), v2 = warp_sum_ll(skips);
+  if (lane == 0) { red[warp * 8 + 0] = (double)v0; red[warp * 8 + 1] = (double)v1; red[warp * 8 + 2] = (double)v2; }
+  __syncthreads();
+  if (tid == 0) {
+    double t0 = 0, t1 = 0, t2 = 0;
+    for (int w = 0; w < W; ++w) { t0 += red[w * 8]; t1 += red[w * 8 + 1]; t2 += red[w * 8 + 2]; }
+    double* sc = out + kd + 2LL * k;
+    for (int i = 0; i < NSCAL; ++i) sc[i] = 0.0;
+    sc[S_REASSIGNED] = t0;
+    sc[S_COMPUTED] = t1;
+    sc[S_SKIPS] = t2;
+  }
+}
+
+constexpr size_t SMEM_MAX = 227 * 1024;
+
+int mti_warps_for(int DP, int k, int d) {
+  for (int W = KNB_WARPS; W >= 1; W >>= 1)
+    if (MtiMmaSmem(DP, k, d, W).total <= SMEM_MAX) return W;
+  return 0;
+}
+
+template <int DP>
+cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
+  const int W = mti_warps_for(DP, a.k, a.d);
+  if (!W) return cudaErrorInvalidValue;
+  const MtiMmaSmem L(DP, a.k, a.d, W);
+  cudaError_t e = cudaFuncSetAttribute(mti_mma_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return e;
+  mti_mma_kernel<DP><<<grid, W * 32, L.total, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool mti_mma_fits(int DP, int k, int d) { return DP >= 4 && DP <= 64 && mti_warps_for(DP, k, d) > 0; }
+
+cudaError_t launch_mti_mma(const MtiArgs& a, int DP, int grid, cudaStream_t s) {
+  switch (DP) {
+    case 4: return launch_dp<4>(a, grid, s);
+    case 8: return launch_dp<8>(a, grid, s);
+    case 16: return launch_dp<16>(a, grid, s);
+    case 32: return launch_dp<32>(a, grid, s);
+    case 64: return launch_dp<64>(a, grid, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace knb

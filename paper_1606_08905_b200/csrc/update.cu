@@ -57,7 +57,8 @@ __global__ void finalize_kernel(const FinalArgs f) {
   double* sums = f.exch + (long long)j * d;
   double cntj = f.exch[kd + j];
   double sqj = f.exch[kd + k + j];
-  if (f.pruning) {  // running totals += this iteration's merged (deltas or full totals)
+  {  // running totals += this iteration's merged vector: full totals on the first pass,
+     // signed deltas of moved rows afterwards (pruned runs: engine.py:371-375)
     double* rs = f.run + (long long)j * d;
     for (int e = lane; e < d; e += 32) rs[e] += sums[e];
     __syncwarp();

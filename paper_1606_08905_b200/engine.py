@@ -39,9 +39,14 @@ class EngineConfig:
     """Knobs for one clustering run -- the reference's fields and defaults (engine.py:59-96).
 
     T, N, task_size and scheduler steer the reference's CPU threads; they are
-    validated identically and have no effect on GPU results.  ``device`` and
-    ``batch`` are additions: the CUDA device of a single-GPU run and how many
-    iterations are queued between host checks of the stop flag.
+    validated identically and have no effect on GPU results.  Additions:
+    ``device`` (CUDA device of a single-GPU run), ``batch`` (iterations queued
+    between host checks of the stop flag) and ``mti_scan`` -- how pruned
+    iterations re-assign the survivors of the point-skip test: "exact" walks
+    candidates with clauses 2/3 like the reference (same dist_comps / pruned_*
+    counters), "dense" scores survivors on the FP64 tensor cores (same
+    assignments, bounds, skips and centroids; dist_comps = k per survivor,
+    pruned_* = 0), "auto" = "dense" where the tensor-core kernel applies.
     """
 
     k: int
@@ -60,6 +65,7 @@ class EngineConfig:
     validate_bounds: bool = False
     device: int | None = None
     batch: int = 16
+    mti_scan: str = "auto"
 
     def validate(self) -> None:
         if self.k < 1:
@@ -82,6 +88,8 @@ class EngineConfig:
             raise ValueError(f"unknown scheduler {self.scheduler!r}")
         if self.batch < 1:
             raise ValueError("batch must be >= 1")
+        if self.mti_scan not in _native.MTI_SCAN:
+            raise ValueError(f"unknown mti_scan {self.mti_scan!r}")
 
 
 @dataclass
@@ -221,6 +229,8 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
     cls = context_cls or _native.Context
     ctx = cls(device, n, n_local, row_lo, d, k, cfg.pruning, cfg.max_iters, cfg.tolerance, stream)
     try:
+        if cfg.mti_scan != "auto":
+            ctx.set_option(_native.KNB_OPT_MTI_SCAN, _native.MTI_SCAN[cfg.mti_scan])
         exch = comm.make_exchange(ctx.exchange_len(), device)
         if exch is not None:
             ctx.set_exchange(exch.data_ptr(), exch.numel())
@@ -315,6 +325,8 @@ class Lloyd:
             stream = torch_stream(device)
         self.ctx = _native.Context(device, self.n, self.n_local, self.row_lo, self.d, cfg.k, cfg.pruning,
                                    cfg.max_iters, cfg.tolerance, stream)
+        if cfg.mti_scan != "auto":
+            self.ctx.set_option(_native.KNB_OPT_MTI_SCAN, _native.MTI_SCAN[cfg.mti_scan])
         self._dev = dev
         self.exch = self.comm.make_exchange(self.ctx.exchange_len(), device)
         if self.exch is not None:

@@ -48,6 +48,9 @@ class FakeContext:
     def close(self):
         pass
 
+    def set_option(self, option, value):
+        self.mti_scan = value
+
     def sync(self):
         pass
 

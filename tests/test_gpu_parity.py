@@ -33,9 +33,10 @@ def _cfg(name, **over):
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_gpu_matches_reference_golden(name):
+    """mti_scan="exact": every output including the reference's work counters."""
     g = golden(name)
     m = case_data(name)
-    r = kb.kmeans(m, _cfg(name, collect_assignments=True))
+    r = kb.kmeans(m, _cfg(name, collect_assignments=True, mti_scan="exact"))
     counters = {key: g[key] for key in COUNTERS}
     assert_parity(m.astype(np.float64), r, g["means"], g["assignments"], len(g["reassignments"]),
                   want_prev=g["prev_means"], counters=counters, wcss=g["wcss"], what=name)
@@ -43,6 +44,26 @@ def test_gpu_matches_reference_golden(name):
     assert [_sha(h) for h in r.assignment_history] == list(g["history_sha"]), name
     np.testing.assert_array_equal(r.centroids.counts, g["counts"])
     assert r.converged == bool(g["converged"])
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if CASES[n]["cfg"].get("pruning", True)])
+def test_gpu_tensor_core_mti_matches_reference_golden(name):
+    """Default mti_scan ("auto" -> tensor-core survivors): assignments every iteration,
+    centroids, bounds-driven skip counts and reassignments are the reference's; the
+    distance count is k per survivor."""
+    g = golden(name)
+    m = case_data(name)
+    r = kb.kmeans(m, _cfg(name, collect_assignments=True))
+    assert_parity(m.astype(np.float64), r, g["means"], g["assignments"], len(g["reassignments"]),
+                  want_prev=g["prev_means"], counters={"reassignments": g["reassignments"], "skips": g["skips"]},
+                  wcss=g["wcss"], what=name)
+    assert [_sha(h) for h in r.assignment_history] == list(g["history_sha"]), name
+    n, d, k = m.shape[0], m.shape[1], int(CASES[name]["cfg"]["k"])
+    assert r.iterations[0].dist_comps == n * k
+    if d <= 64:  # the tensor-core survivor kernel (wider rows keep the exact walk)
+        for s in r.iterations[1:]:
+            assert s.dist_comps == (n - s.skips) * k
+            assert s.pruned_stale == 0 and s.pruned_tight == 0
 
 
 @pytest.mark.parametrize("name", ["c1_full", "c3_mini", "kpp_pruned", "d33_pruned", "d65_dense"])
@@ -93,6 +114,9 @@ def test_pruned_equals_dense_every_iteration(seed):
     assert np.max(np.abs(p.centroids.means - q.centroids.means)) < 1e-9
     o = O.lloyd(m, k, seed=seed + 1, max_iters=8, pruning=True)
     assert_parity(m, p, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
+                  counters={key: [getattr(s, key) for s in o.iterations] for key in ("reassignments", "skips")})
+    x = kb.kmeans(m, kb.EngineConfig(pruning=True, mti_scan="exact", **base))
+    assert_parity(m, x, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
                   counters={key: [getattr(s, key) for s in o.iterations] for key in COUNTERS})
 
 
@@ -100,7 +124,7 @@ def test_large_k_generic_path():
     """k*d too large for shared memory -> generic kernels, same answers."""
     m = kb.synth.uniform(6000, 16, 77)
     cfg = dict(k=2000, seed=3, max_iters=3)
-    r = kb.kmeans(m, kb.EngineConfig(pruning=True, **cfg))
+    r = kb.kmeans(m, kb.EngineConfig(pruning=True, mti_scan="exact", **cfg))
     o = O.lloyd(m, 2000, seed=3, max_iters=3, pruning=True)
     assert_parity(m, r, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
                   counters={key: [getattr(s, key) for s in o.iterations] for key in COUNTERS})
