@@ -222,15 +222,10 @@ __global__ void __launch_bounds__(KNB_NT, 1)
       ++rows_done;
     }
     if (!a.delta) {
-      accumulate_rows<DP>(valid ? ((unsigned)id << 5) | (unsigned)my_r : 0xffffffffu, my_sq, 1.0, tb, acc, cnt,
-                          sqa, d, lane);
+      accumulate_in_row_order<DP>(row_mask(valid, my_r), id, -1, my_sq, tb, acc, cnt, sqa, d, lane);
     } else {
       // steady-state dense passes: running sums move by the reassigned rows only
-      const bool moved = valid && id != old;
-      accumulate_rows<DP>(moved ? ((unsigned)id << 5) | (unsigned)my_r : 0xffffffffu, 0.0, 1.0, tb, acc, cnt, sqa,
-                          d, lane);
-      accumulate_rows<DP>(moved ? ((unsigned)old << 5) | (unsigned)my_r : 0xffffffffu, 0.0, -1.0, tb, acc, cnt,
-                          sqa, d, lane);
+      accumulate_in_row_order<DP>(row_mask(valid && id != old, my_r), id, old, 0.0, tb, acc, cnt, sqa, d, lane);
     }
     // ---- refill this stage with the block NS strides ahead
     __syncwarp();

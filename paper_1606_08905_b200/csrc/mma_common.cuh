@@ -103,43 +103,31 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
     bid[pg] = 0;
     flag[pg] = false;
   }
-#pragma unroll 1
-  for (int cb = 0; cb < ntile8; cb += 4) {
-    const int nq = ntile8 - cb < 4 ? ntile8 - cb : 4;
-    double c[4][4][2];
+  // Centroid-tile-major: for each 8-centroid tile, 4 independent accumulator chains
+  // (one per 8-row group) run d/4 k-steps; that tile's epilogue only depends on its own
+  // chains, so ptxas overlaps it with the next tile's DMMAs.
+#pragma unroll 2
+  for (int q = 0; q < ntile8; ++q) {
+    const double2 h = *reinterpret_cast<const double2*>(chn + q * 8 + 2 * t4);
+    double c[4][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double2 h = q < nq ? *reinterpret_cast<const double2*>(chn + (cb + q) * 8 + 2 * t4) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int pg = 0; pg < 4; ++pg) { c[pg][q][0] = h.x; c[pg][q][1] = h.y; }
-    }
+    for (int pg = 0; pg < 4; ++pg) { c[pg][0] = h.x; c[pg][1] = h.y; }
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      double av[4];
+      const double bv = bf[((q * KS + ks) << 5) + lane];
 #pragma unroll
       for (int pg = 0; pg < 4; ++pg) {
-        if constexpr (ACACHE) av[pg] = afr[pg][ks];
-        else av[pg] = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q < nq) {
-          const double bv = bf[(((cb + q) * KS + ks) << 5) + lane];
-#pragma unroll
-          for (int pg = 0; pg < 4; ++pg) dmma(c[pg][q], av[pg], bv);
-        }
+        double av;
+        if constexpr (ACACHE) av = afr[pg][ks];
+        else av = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
+        dmma(c[pg], av, bv);
       }
     }
+    const int j0 = q * 8 + 2 * t4;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q < nq) {
-        const int j0 = (cb + q) * 8 + 2 * t4;
-#pragma unroll
-        for (int pg = 0; pg < 4; ++pg) {
-          score_update(best[pg], bid[pg], flag[pg], c[pg][q][0], j0, tolhi[pg]);
-          score_update(best[pg], bid[pg], flag[pg], c[pg][q][1], j0 + 1, tolhi[pg]);
-        }
-      }
+    for (int pg = 0; pg < 4; ++pg) {
+      score_update(best[pg], bid[pg], flag[pg], c[pg][0], j0, tolhi[pg]);
+      score_update(best[pg], bid[pg], flag[pg], c[pg][1], j0 + 1, tolhi[pg]);
     }
   }
 #pragma unroll
@@ -182,6 +170,53 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
   }
   if (sq_out) *sq_out = exact_sq<DP>(x, Zero{}, d);
   return nd;
+}
+
+// Deterministic warp-local accumulation in row order, lanes = dims.  For every row r
+// set in `rowmask` (ascending; the row's values live in lane owner_lane(r)):
+//   acc[to][e] += x[r][e], cnt[to] += 1, sqa[to] += sq, and when from >= 0 the same
+//   amounts are subtracted from cluster `from` (a moved row's signed delta,
+//   engine.py:345-353).  Full passes pass every valid row with from = -1.
+template <int DP>
+__device__ __forceinline__ void accumulate_in_row_order(unsigned rowmask, int to, int from, double sq,
+                                                        const unsigned char* tb, double* acc, double* cnt,
+                                                        double* sqa, int d, int lane) {
+  using TL = TileLayout<DP>;
+  const int e0 = lane < d ? lane : 0;
+  const int e1 = lane + 32 < d ? lane + 32 : 0;
+  while (rowmask) {
+    const int r = __ffs(rowmask) - 1;
+    rowmask &= rowmask - 1;
+    const int src = owner_lane(r);
+    const int t = __shfl_sync(0xffffffffu, to, src);
+    const int f = __shfl_sync(0xffffffffu, from, src);
+    const double q = __shfl_sync(0xffffffffu, sq, src);
+    const double x0 = *reinterpret_cast<const double*>(tb + TL::elem_off(r, e0, BR));
+    if (lane < d) {
+      acc[t * d + lane] += x0;
+      if (f >= 0) acc[f * d + lane] -= x0;
+    }
+    if constexpr (DP > 32) {
+      const double x1 = *reinterpret_cast<const double*>(tb + TL::elem_off(r, e1, BR));
+      if (lane + 32 < d) {
+        acc[t * d + lane + 32] += x1;
+        if (f >= 0) acc[f * d + lane + 32] -= x1;
+      }
+    }
+    if (lane == 0) {
+      cnt[t] += 1.0;
+      sqa[t] += q;
+      if (f >= 0) {
+        cnt[f] -= 1.0;
+        sqa[f] -= q;
+      }
+    }
+  }
+}
+
+// Bit r set when the lane owning row r (owner_lane(r)) passes `pred`.
+__device__ __forceinline__ unsigned row_mask(bool pred, int my_row) {
+  return __reduce_or_sync(0xffffffffu, pred ? (1u << my_row) : 0u);
 }
 
 // Deterministic warp-local accumulation of the block rows selected by `key`

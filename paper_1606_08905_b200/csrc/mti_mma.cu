@@ -147,9 +147,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
       }
     }
     if (lane == 0) computed += (long long)cnum * k;
-    accumulate_rows<DP>(moved ? ((unsigned)id << 5) | (unsigned)r : 0xffffffffu, sq, 1.0, tb, acc, cnt, sqa, d, lane);
-    accumulate_rows<DP>(moved ? ((unsigned)orig << 5) | (unsigned)r : 0xffffffffu, sq, -1.0, tb, acc, cnt, sqa, d,
-                        lane);
+    accumulate_in_row_order<DP>(row_mask(moved, r), id, orig, sq, tb, acc, cnt, sqa, d, lane);
     __syncwarp();
   };
 
