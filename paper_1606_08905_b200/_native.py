@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libknorb200.so")
+LIB_PATH = os.environ.get("KNB_LIB") or os.path.join(HERE, "libknorb200.so")  # KNB_LIB: experiments only
 
 KNB_E_ARG, KNB_E_CUDA, KNB_E_STATE, KNB_E_COUNT, KNB_E_NOMEM = -1, -2, -3, -4, -5
 KNB_OPT_MTI_SCAN = 1

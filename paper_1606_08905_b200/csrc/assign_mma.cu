@@ -190,9 +190,12 @@ __global__ void __launch_bounds__(KNB_NT, 1)
     const int my_r = t4 * 8 + g;  // the row this lane finishes after the quad combine
     const bool valid = row0 + my_r < a.n;
     const long long row = row0 + my_r;
-    int id = 0, old = -1;
+    int id = 0;
     double my_sq = 0.0;
-    if (valid) old = a.assign[row];
+    // unconditional (clamped) load: its latency hides behind score_block instead of
+    // stalling the block start at a reconvergence point
+    const int old_raw = a.assign[valid ? row : 0];
+    int old = -1;
     if (!labels) {
       const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
       id = sc.id;
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(KNB_NT, 1)
         // certified winner: WCSS term from the norm form ||x||^2 - 2 s (rounding ~1e-16 ||x||^2)
         nd2 = fmax(sc.xn2 - 2.0 * sc.best, 0.0);
       }
+      old = valid ? old_raw : -1;
       if (valid) {
         if (id != old) {
           a.assign[row] = id;
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(KNB_NT, 1)
         ++rows_done;
       }
     } else if (valid) {
+      old = old_raw;
       id = old;
       ++rows_done;
     }

@@ -7,18 +7,29 @@
 
 #include "common.cuh"
 
+#ifndef KNB_EXPERIMENT
+#define KNB_EXPERIMENT 0
+#endif
+
 namespace knb {
 
 constexpr int BR = 32;  // rows per warp block
 
+// not volatile: the mma has no side effects, so ptxas may interleave it with the epilogue
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
+#if KNB_EXPERIMENT == 2  // experiment: no tensor work
+  c[0] += a; c[1] += b; return;
+#endif
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
 }
 
 // running argmax with the near-tie flag; integer ops on the high word of s - best
 __device__ __forceinline__ void score_update(double& best, int& bid, bool& flag, double s, int j, int tolhi) {
+#if KNB_EXPERIMENT == 1  // experiment: no epilogue (keep the value live)
+  best = fmax(best, s); return;
+#endif
   const double diff = __dsub_rn(s, best);
   const int h = __double2hiint(diff);
   const bool better = h > 0;
@@ -106,30 +117,56 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
   // Centroid-tile-major: for each 8-centroid tile, 4 independent accumulator chains
   // (one per 8-row group) run d/4 k-steps; that tile's epilogue only depends on its own
   // chains, so ptxas overlaps it with the next tile's DMMAs.
-#pragma unroll 2
-  for (int q = 0; q < ntile8; ++q) {
-    const double2 h = *reinterpret_cast<const double2*>(chn + q * 8 + 2 * t4);
-    double c[4][2];
+  // Two tiles per step (8 independent chains), software-pipelined: the DMMAs of step
+  // q+2 are issued before the epilogue of step q, so the tensor pipe works while the
+  // epilogue's dependent integer chain runs.  An odd tile count pads with a dummy
+  // tile whose chn is -inf (never wins, never near).
+  auto mma_step = [&](int q, double (&c0)[4][2], double (&c1)[4][2]) {
+    const bool two = q + 1 < ntile8;
+    const double2 h0 = *reinterpret_cast<const double2*>(chn + q * 8 + 2 * t4);
+    const double2 h1 = two ? *reinterpret_cast<const double2*>(chn + (q + 1) * 8 + 2 * t4)
+                           : make_double2(-CUDART_INF, -CUDART_INF);
 #pragma unroll
-    for (int pg = 0; pg < 4; ++pg) { c[pg][0] = h.x; c[pg][1] = h.y; }
+    for (int pg = 0; pg < 4; ++pg) {
+      c0[pg][0] = h0.x; c0[pg][1] = h0.y;
+      c1[pg][0] = h1.x; c1[pg][1] = h1.y;
+    }
+    const int q1 = two ? q + 1 : q;  // a valid fragment address for the dummy tile
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      const double bv = bf[((q * KS + ks) << 5) + lane];
+      const double bv0 = bf[((q * KS + ks) << 5) + lane];
+      const double bv1 = bf[((q1 * KS + ks) << 5) + lane];
 #pragma unroll
       for (int pg = 0; pg < 4; ++pg) {
         double av;
         if constexpr (ACACHE) av = afr[pg][ks];
         else av = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
-        dmma(c[pg], av, bv);
+        dmma(c0[pg], av, bv0);
+        dmma(c1[pg], av, bv1);
       }
     }
+  };
+  auto epilogue = [&](int q, const double (&c0)[4][2], const double (&c1)[4][2]) {
     const int j0 = q * 8 + 2 * t4;
 #pragma unroll
     for (int pg = 0; pg < 4; ++pg) {
-      score_update(best[pg], bid[pg], flag[pg], c[pg][0], j0, tolhi[pg]);
-      score_update(best[pg], bid[pg], flag[pg], c[pg][1], j0 + 1, tolhi[pg]);
+      score_update(best[pg], bid[pg], flag[pg], c0[pg][0], j0, tolhi[pg]);
+      score_update(best[pg], bid[pg], flag[pg], c0[pg][1], j0 + 1, tolhi[pg]);
+      score_update(best[pg], bid[pg], flag[pg], c1[pg][0], j0 + 8, tolhi[pg]);
+      score_update(best[pg], bid[pg], flag[pg], c1[pg][1], j0 + 9, tolhi[pg]);
     }
+  };
+  double ca0[4][2], ca1[4][2], cb0[4][2], cb1[4][2];
+  mma_step(0, ca0, ca1);
+  int q = 0;
+#pragma unroll 1
+  for (; q + 2 < ntile8; q += 4) {
+    mma_step(q + 2, cb0, cb1);
+    epilogue(q, ca0, ca1);
+    if (q + 4 < ntile8) mma_step(q + 4, ca0, ca1);
+    epilogue(q + 2, cb0, cb1);
   }
+  if (q < ntile8) epilogue(q, ca0, ca1);
 #pragma unroll
   for (int pg = 0; pg < 4; ++pg) {
     combine(best[pg], bid[pg], flag[pg], tolhi[pg], 1);

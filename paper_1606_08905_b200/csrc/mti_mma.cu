@@ -49,7 +49,7 @@ struct MtiMmaSmem {
     size_t w = 0;
     tile_stride = (size_t)BR * DP * 8;
     tile_off = w; w += 2 * tile_stride;  // two staging tiles (gather double buffer)
-    q_off = w;    w += 96 * 4 * 2;       // queued rows and their pre-scan assignment
+    q_off = w;    w += 192 * 4 * 2;      // queued rows and their pre-scan assignment
     acc_off = w;  w += (size_t)k * d * 8;
     cnt_off = w;  w += (size_t)k * 8;
     sq_off = w;   w += (size_t)k * 8;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   unsigned char* wbase = smem + L.warp0 + (size_t)warp * L.per_warp;
   unsigned char* tb = wbase + L.tile_off;
   int* qrow = reinterpret_cast<int*>(wbase + L.q_off);
-  int* qorig = qrow + 96;
+  int* qorig = qrow + 192;
   double* acc = reinterpret_cast<double*>(wbase + L.acc_off);
   double* cnt = reinterpret_cast<double*>(wbase + L.cnt_off);
   double* sqa = reinterpret_cast<double*>(wbase + L.sq_off);
@@ -153,31 +153,44 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 
   // filter strided blocks (bound inflation + clause 1) until `target` survivors are queued
   long long blk = gw;
+  // (state loads for FB blocks are issued together so their latency overlaps)
+  constexpr int FB = 4;
   auto filter_until = [&](int target) {
     while (qn < target && blk < nblk) {
-      const long long row = blk * BR + lane;
-      bool live = false;
-      int aa = 0;
-      if (row < a.n) {
-        aa = a.assign[row];
-        double u = a.upper[row];
-        const double dr = drift[aa];
-        if (dr != 0.0) {  // u + 0.0 == u and tight & true == tight: no store needed
-          u = u + dr;
-          a.upper[row] = u;
-          a.tight[row] = 0;
+      int aa[FB];
+      double uu[FB];
+#pragma unroll
+      for (int j = 0; j < FB; ++j) {
+        const long long row = (blk + j * TW) * BR + lane;
+        const bool ok = blk + j * TW < nblk && row < a.n;
+        aa[j] = ok ? a.assign[row] : -1;
+        uu[j] = ok ? a.upper[row] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < FB; ++j) {
+        if (blk + j * TW >= nblk) break;  // uniform
+        const long long row = (blk + j * TW) * BR + lane;
+        bool live = false;
+        if (aa[j] >= 0) {
+          double u = uu[j];
+          const double dr = drift[aa[j]];
+          if (dr != 0.0) {  // u + 0.0 == u and tight & true == tight: no store needed
+            u = u + dr;
+            a.upper[row] = u;
+            a.tight[row] = 0;
+          }
+          if (u <= hmin[aa[j]]) ++skips;
+          else live = true;
         }
-        if (u <= hmin[aa]) ++skips;
-        else live = true;
+        const unsigned b = __ballot_sync(0xffffffffu, live);
+        if (live) {
+          const int pos = qn + __popc(b & ((1u << lane) - 1u));
+          qrow[pos] = (int)row;
+          qorig[pos] = aa[j];
+        }
+        qn += __popc(b);
       }
-      const unsigned b = __ballot_sync(0xffffffffu, live);
-      if (live) {
-        const int pos = qn + __popc(b & ((1u << lane) - 1u));
-        qrow[pos] = (int)row;
-        qorig[pos] = aa;
-      }
-      qn += __popc(b);
-      blk += TW;
+      blk += FB * TW;
       __syncwarp();
     }
   };

@@ -59,6 +59,16 @@ int main() {
     double fmas = (double)sms * bpsm * 256 * 8 * it;
     printf("dfma  blocks/SM=%d: %.2f T FMA/s (%.1f TFLOP/s)\n", bpsm, fmas / ms / 1e9, 2 * fmas / ms / 1e9);
   }
+  for (int bpsm : {1}) {
+    for (int thr : {128, 256}) {
+      float ms = timeit([&] { dmma_k<8><<<sms * bpsm, thr>>>(out, it); });
+      double fmas = (double)sms * bpsm * (thr / 32) * 256 * 8 * it;
+      printf("dmma8 1 block/SM of %d threads (%d warps/SM): %.2f T FMA/s\n", thr, thr / 32, fmas / ms / 1e9);
+      ms = timeit([&] { dmma_k<16><<<sms * bpsm, thr>>>(out, it); });
+      fmas = (double)sms * bpsm * (thr / 32) * 256 * 16 * it;
+      printf("dmma16 1 block/SM of %d threads (%d warps/SM): %.2f T FMA/s\n", thr, thr / 32, fmas / ms / 1e9);
+    }
+  }
   for (int bpsm : {2, 4, 8}) {
     float ms = timeit([&] { dmma_k<4><<<sms * bpsm, 256>>>(out, it); });
     double fmas = (double)sms * bpsm * 8 * 256 * 4 * it;
