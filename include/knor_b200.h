@@ -142,6 +142,13 @@ int knb_state_bytes(knb_ctx* ctx, int64_t* bytes);
  * (grid_mti < 0: the tensor-core MTI kernel with -grid_mti CTAs). */
 int knb_describe(knb_ctx* ctx, int32_t* dense_dp, int32_t* use_tma, int32_t* grid_dense, int32_t* grid_mti);
 
+/* numpy's default_rng(seed).random(...) on the device: writes draws [first_draw,
+ * first_draw + count) of the PCG64 stream whose (state, inc) the host read from
+ * Generator.bit_generator.state into dev_out, bit-identical to the host stream (config 4's
+ * U[0,1)^16 input).  Context-free; stream may be NULL. */
+int knb_fill_uniform_pcg64(double* dev_out, int64_t count, int64_t first_draw, uint64_t state_hi,
+                           uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, void* stream);
+
 /* Roofline denominators measured on the device: FP64 FMA rate (DFMA/s, 8 independent chains
  * per thread over 8 CTAs/SM) and a 1 GiB device copy (read + write bytes/s). */
 int knb_measure_peaks(int device, double* dfma_per_s, double* copy_bytes_per_s);

@@ -84,6 +84,7 @@ SIGNATURES = {
     "knb_describe": [_P, _PI32, _PI32, _PI32, _PI32],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
     "knb_set_option": [_P, _I32, _I64],
+    "knb_fill_uniform_pcg64": [_P, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P],
 }
 
 _lib = None

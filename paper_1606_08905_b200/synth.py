@@ -11,6 +11,7 @@ concatenation of sequential chunk draws).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -70,6 +71,28 @@ def uniform(n: int, d: int, seed: int, chunk_rows: int = 1 << 20, dtype="float64
         b = min(a + chunk_rows, n)
         x[a:b] = rng.random((b - a, d))
     return x
+
+
+def uniform_device(n: int, d: int, seed: int, row_lo: int = 0, rows: int | None = None, device: int = 0):
+    """Rows [row_lo, row_lo + rows) of ``default_rng(seed).random((n, d))`` generated
+    in HBM by the PCG64 kernel (bit-identical to the host stream) -> CUDA tensor."""
+    import torch
+
+    from . import _native
+
+    rows = n - row_lo if rows is None else rows
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    out = torch.empty((rows, d), dtype=torch.float64, device=torch.device("cuda", device))
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream().cuda_stream or 1
+        rc = _native.lib().knb_fill_uniform_pcg64(
+            ctypes.c_void_p(out.data_ptr()), rows * d, row_lo * d, s >> 64, s & m64, inc >> 64, inc & m64,
+            ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(f"knb_fill_uniform_pcg64 failed ({rc})")
+    return out
 
 
 # BASELINE.json configs; seed = config index (BASELINE.md section 4).
