@@ -128,13 +128,17 @@ int knb_set_ignore_stop(knb_ctx* ctx, int32_t on);
 /* Options.  KNB_OPT_MTI_SCAN selects how a pruned iteration re-assigns the survivors of the
  * point-skip test (clause 1): KNB_MTI_EXACT walks the candidates with clauses 2/3 exactly like
  * scan_block (pruning.py:163-204), reproducing its dist_comps / pruned_* counters;
- * KNB_MTI_DENSE scores survivors on the FP64 tensor cores (certified argmin, exact bound) --
- * identical assignments, bounds, skips and centroids, dist_comps = k per survivor;
- * KNB_MTI_AUTO (default) = DENSE where available (d <= 64, centroids fit shared memory). */
+ * KNB_MTI_DENSE compacts survivors per warp and scores them on the FP64 tensor cores
+ * (certified argmin, exact bound) -- identical assignments, bounds, skips and centroids,
+ * dist_comps = k per survivor; KNB_MTI_BLOCK streams every block through the tensor-core
+ * pass and skips only blocks whose rows all pass clause 1 (same outputs); KNB_MTI_AUTO
+ * (default, d <= 64 and centroids in shared memory) picks BLOCK or DENSE on the device each
+ * iteration from the previous iteration's skip fraction. */
 #define KNB_OPT_MTI_SCAN 1
 #define KNB_MTI_AUTO 0
 #define KNB_MTI_EXACT 1
 #define KNB_MTI_DENSE 2
+#define KNB_MTI_BLOCK 3
 int knb_set_option(knb_ctx* ctx, int32_t option, int64_t value);
 /* Device bytes held by the context (the GPU analogue of KmeansResult.peak_state_bytes). */
 int knb_state_bytes(knb_ctx* ctx, int64_t* bytes);

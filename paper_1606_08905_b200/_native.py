@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("KNB_LIB") or os.path.join(HERE, "libknorb200.so")  # 
 
 KNB_E_ARG, KNB_E_CUDA, KNB_E_STATE, KNB_E_COUNT, KNB_E_NOMEM = -1, -2, -3, -4, -5
 KNB_OPT_MTI_SCAN = 1
-MTI_SCAN = {"auto": 0, "exact": 1, "dense": 2}
+MTI_SCAN = {"auto": 0, "exact": 1, "dense": 2, "block": 3}
 
 
 class NativeUnavailable(RuntimeError):

@@ -52,7 +52,7 @@ __host__ __device__ inline int stages_for(int DP) { return DP <= 8 ? 4 : 2; }
 
 // shared memory: [centroids: bf, crow, chn] [per warp: NS stages, mbar, acc, cnt, sq]
 struct WarpSmem {
-  size_t bf, crow, chn, warp0, stage_bytes, mbar_off, acc_off, cnt_off, sq_off, per_warp, red, total;
+  size_t bf, crow, chn, hmin, drift, warp0, stage_bytes, mbar_off, acc_off, cnt_off, sq_off, per_warp, red, total;
   __host__ __device__ WarpSmem(int DP, int k, int d, int W) {
     const int kp = (k + 7) & ~7;
     const int NS = stages_for(DP);
@@ -60,6 +60,8 @@ struct WarpSmem {
     bf = o;   o += (size_t)kp * DP * 8;
     crow = o; o += (size_t)kp * DP * 8;
     chn = o;  o += (size_t)kp * 8;
+    hmin = o; o += (size_t)k * 8;
+    drift = o; o += (size_t)k * 8;
     red = o;  o += 32 * 4 * 8;
     o = al(o, 1024);
     warp0 = o;
@@ -114,12 +116,15 @@ __global__ void __launch_bounds__(KNB_NT, 1)
   constexpr int NS = DP <= 8 ? 4 : 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
+  if (a.gate && a.ctrl->mti_choice != 1) return;  // the compacted MTI kernel runs this iteration
 
   const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
   const WarpSmem L(DP, k, d, W);
+  double* hmin_s = reinterpret_cast<double*>(smem + L.hmin);
+  double* drift_s = reinterpret_cast<double*>(smem + L.drift);
   double* bf = reinterpret_cast<double*>(smem + L.bf);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
   double* chn = reinterpret_cast<double*>(smem + L.chn);
@@ -142,6 +147,11 @@ __global__ void __launch_bounds__(KNB_NT, 1)
     bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
   }
   for (int j = tid; j < kp; j += blockDim.x) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
+  if (a.mti_filter)
+    for (int j = tid; j < k; j += blockDim.x) {
+      hmin_s[j] = a.half_min[j];
+      drift_s[j] = a.drift[j];
+    }
   for (int i = lane; i < k * d; i += 32) acc[i] = 0.0;
   for (int j = lane; j < k; j += 32) { cnt[j] = 0.0; sqa[j] = 0.0; }
   if (!tma && d < DP) {  // cp.async never writes the padded columns: zero them once
@@ -162,15 +172,28 @@ __global__ void __launch_bounds__(KNB_NT, 1)
   const double tolk = (8.0 * d + 32.0) * 1.1102230246251565e-16;  // (8d+32) * 2^-53
   const long long nblk = (a.n + BR - 1) / BR;
   const long long gw = (long long)blockIdx.x * W + warp, TW = (long long)gridDim.x * W;
-  long long reassigned = 0, rows_done = 0;
+  long long reassigned = 0, rows_done = 0, skips = 0, computed = 0;
   double wcss = 0.0;
 
 #pragma unroll
   for (int s = 0; s < NS; ++s)
     if (gw + s * TW < nblk) load_block<DP>(&tmap, &bar[s], wbase + s * L.stage_bytes, gw + s * TW, a, tma, lane);
 
+  // Per-row state (previous assignment, MTI bound) is prefetched one block ahead so
+  // no block starts by waiting on a global load.
+  const int my_r0 = t4 * 8 + g;
+  auto state_row = [&](long long b) -> long long {
+    const long long r = b * BR + my_r0;
+    return (b < nblk && r < a.n) ? r : 0;
+  };
+  int pf_old = a.assign[state_row(gw)];
+  double pf_u = a.mti_filter ? a.upper[state_row(gw)] : 0.0;
   int it = 0;
   for (long long blk = gw; blk < nblk; blk += TW, ++it) {
+    const int old_raw = pf_old;
+    const double u_pre = pf_u;
+    pf_old = a.assign[state_row(blk + TW)];
+    if (a.mti_filter) pf_u = a.upper[state_row(blk + TW)];
     const int s = it % NS;
     unsigned char* tb = wbase + s * L.stage_bytes;
     if (tma) {
@@ -192,11 +215,40 @@ __global__ void __launch_bounds__(KNB_NT, 1)
     const long long row = row0 + my_r;
     int id = 0;
     double my_sq = 0.0;
-    // unconditional (clamped) load: its latency hides behind score_block instead of
-    // stalling the block start at a reconvergence point
-    const int old_raw = a.assign[valid ? row : 0];
     int old = -1;
-    if (!labels) {
+    if (a.mti_filter) {
+      // block-dense MTI pass: bound inflation + clause 1 per row (pruning.py:152-160,
+      // engine.py:327); survivors get the certified argmin, the exact-recipe bound and
+      // tight = 1 (scan_block's outcome); skipped rows are left exactly as the
+      // reference leaves them.  A block whose rows all skip costs no tensor work.
+      const int aa = valid ? old_raw : 0;
+      double u = u_pre;
+      const double dr = drift_s[aa];
+      if (valid && dr != 0.0) {
+        u = u + dr;
+        a.upper[row] = u;
+        a.tight[row] = 0;
+      }
+      const bool live = valid && !(u <= hmin_s[aa]);
+      skips += (valid && !live) ? 1 : 0;
+      const unsigned lmask = __ballot_sync(0xffffffffu, live);
+      if (lmask) {
+        const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+        int nid = sc.id;
+        double sq = 0.0;
+        const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, &sq);
+        if (live) {
+          a.upper[row] = nd;
+          a.tight[row] = 1;
+          if (nid != aa) {
+            a.assign[row] = nid;
+            ++reassigned;
+          }
+        }
+        if (lane == 0) computed += (long long)__popc(lmask) * k;
+        accumulate_in_row_order<DP>(row_mask(live && nid != aa, my_r), nid, aa, sq, tb, acc, cnt, sqa, d, lane);
+      }
+    } else if (!labels) {
       const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
       id = sc.id;
       double nd2;
@@ -226,7 +278,9 @@ __global__ void __launch_bounds__(KNB_NT, 1)
       id = old;
       ++rows_done;
     }
-    if (!a.delta) {
+    if (a.mti_filter) {
+      // accumulated above
+    } else if (!a.delta) {
       accumulate_in_row_order<DP>(row_mask(valid, my_r), id, -1, my_sq, tb, acc, cnt, sqa, d, lane);
     } else {
       // steady-state dense passes: running sums move by the reassigned rows only
@@ -259,16 +313,31 @@ __global__ void __launch_bounds__(KNB_NT, 1)
   const double r_re = (double)warp_sum_ll(reassigned);
   const double r_w = warp_sum(wcss);
   const double r_rows = (double)warp_sum_ll(rows_done);
-  if (lane == 0) { red[warp * 4 + 0] = r_re; red[warp * 4 + 1] = r_w; red[warp * 4 + 2] = r_rows; }
+  const double r_sk = (double)warp_sum_ll(skips);
+  const double r_cp = (double)warp_sum_ll(computed);
+  if (lane == 0) {
+    red[warp * 8 + 0] = r_re;
+    red[warp * 8 + 1] = r_w;
+    red[warp * 8 + 2] = r_rows;
+    red[warp * 8 + 3] = r_sk;
+    red[warp * 8 + 4] = r_cp;
+  }
   __syncthreads();
   if (tid == 0) {
-    double t_re = 0, t_w = 0, t_rows = 0;
-    for (int w = 0; w < W; ++w) { t_re += red[w * 4]; t_w += red[w * 4 + 1]; t_rows += red[w * 4 + 2]; }
+    double t_re = 0, t_w = 0, t_rows = 0, t_sk = 0, t_cp = 0;
+    for (int w = 0; w < W; ++w) {
+      t_re += red[w * 8];
+      t_w += red[w * 8 + 1];
+      t_rows += red[w * 8 + 2];
+      t_sk += red[w * 8 + 3];
+      t_cp += red[w * 8 + 4];
+    }
     double* sc = out + kd + 2LL * k;
     for (int i = 0; i < NSCAL; ++i) sc[i] = 0.0;
     sc[S_REASSIGNED] = t_re;
     sc[S_WCSS] = t_w;
-    sc[S_COMPUTED] = labels ? 0.0 : t_rows * (double)k;
+    sc[S_COMPUTED] = a.mti_filter ? t_cp : (labels ? 0.0 : t_rows * (double)k);
+    sc[S_SKIPS] = t_sk;
     sc[S_ROWS] = t_rows;
   }
 }

@@ -173,52 +173,78 @@ int need_ready(knb_ctx* c, bool centroids) {
   return KNB_OK;
 }
 
+DenseArgs dense_args(knb_ctx* c) {
+  DenseArgs a;
+  a.X = c->X;
+  a.n = c->n_local;
+  a.d = c->d;
+  a.k = c->k;
+  a.assign = c->assign;
+  a.upper = c->upper;
+  a.tight = c->tight;
+  a.mti_seed = 0;
+  a.labels_only = 0;
+  a.delta = 0;
+  a.mti_filter = 0;
+  a.gate = 0;
+  a.drift = c->drift;
+  a.half_min = c->half_min;
+  a.means = c->means;
+  a.chn = c->chn;
+  a.partials = c->partials;
+  a.ctrl = c->ctrl;
+  a.use_tma = c->use_tma;
+  return a;
+}
+
 int launch_local(knb_ctx* c) {
   const bool full = !c->pruning || c->t_host == 0;
   if (full) {
-    DenseArgs a;
-    a.X = c->X;
-    a.n = c->n_local;
-    a.d = c->d;
-    a.k = c->k;
-    a.assign = c->assign;
-    a.upper = c->upper;
-    a.tight = c->tight;
+    DenseArgs a = dense_args(c);
     a.mti_seed = c->pruning;
-    a.labels_only = 0;
     a.delta = (!c->pruning && c->t_host > 0) ? 1 : 0;
-    a.means = c->means;
-    a.chn = c->chn;
-    a.partials = c->partials;
-    a.ctrl = c->ctrl;
-    a.use_tma = c->use_tma;
     KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
     KNB_CUDA(launch_reduce(c->partials, c->G_dense, c->L, c->exch, c->ctrl, c->stream));
-  } else {
-    MtiArgs a;
-    a.X = c->X;
-    a.n = c->n_local;
-    a.d = c->d;
-    a.k = c->k;
-    a.assign = c->assign;
-    a.upper = c->upper;
-    a.tight = c->tight;
-    a.means = c->means;
-    a.drift = c->drift;
-    a.half = c->half;
-    a.half_min = c->half_min;
-    a.chn = c->chn;
-    a.partials = c->partials;
-    a.ctrl = c->ctrl;
-    a.half_in_smem = c->half_in_smem;
-    if (c->mti_scan != KNB_MTI_EXACT && c->mti_mma_ok) {
-      KNB_CUDA(launch_mti_mma(a, c->DP, c->G_mti_mma, c->stream));
-      KNB_CUDA(launch_reduce(c->partials, c->G_mti_mma, c->L, c->exch, c->ctrl, c->stream));
-    } else {
-      KNB_CUDA(launch_mti(a, c->DPm, c->G_mti, c->stream));
-      KNB_CUDA(launch_reduce(c->partials, c->G_mti, c->L, c->exch, c->ctrl, c->stream));
-    }
+    return KNB_OK;
   }
+  MtiArgs m;
+  m.X = c->X;
+  m.n = c->n_local;
+  m.d = c->d;
+  m.k = c->k;
+  m.assign = c->assign;
+  m.upper = c->upper;
+  m.tight = c->tight;
+  m.means = c->means;
+  m.drift = c->drift;
+  m.half = c->half;
+  m.half_min = c->half_min;
+  m.chn = c->chn;
+  m.partials = c->partials;
+  m.ctrl = c->ctrl;
+  m.half_in_smem = c->half_in_smem;
+  m.gate = 0;
+  const int mode = c->mti_mma_ok ? c->mti_scan : KNB_MTI_EXACT;
+  if (mode == KNB_MTI_EXACT) {
+    KNB_CUDA(launch_mti(m, c->DPm, c->G_mti, c->stream));
+    KNB_CUDA(launch_reduce(c->partials, c->G_mti, c->L, c->exch, c->ctrl, c->stream));
+    return KNB_OK;
+  }
+  DenseArgs a = dense_args(c);
+  a.mti_filter = 1;
+  if (mode == KNB_MTI_BLOCK) {
+    KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
+  } else if (mode == KNB_MTI_DENSE) {
+    KNB_CUDA(launch_mti_mma(m, c->DP, c->G_dense, c->stream));
+  } else {
+    // auto: both are queued; the device-side choice made by the previous finalize
+    // (skip fraction) lets exactly one of them run, the other returns at once
+    a.gate = 1;
+    m.gate = 1;
+    KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
+    KNB_CUDA(launch_mti_mma(m, c->DP, c->G_dense, c->stream));
+  }
+  KNB_CUDA(launch_reduce(c->partials, c->G_dense, c->L, c->exch, c->ctrl, c->stream));
   return KNB_OK;
 }
 
@@ -495,22 +521,8 @@ int knb_init_partition_local(knb_ctx* c, const int32_t* labels) {
   if (rc) return rc;
   if (c->n_local)
     KNB_CUDA(cudaMemcpyAsync(c->assign, labels, sizeof(int32_t) * c->n_local, cudaMemcpyHostToDevice, c->stream));
-  DenseArgs a;
-  a.X = c->X;
-  a.n = c->n_local;
-  a.d = c->d;
-  a.k = c->k;
-  a.assign = c->assign;
-  a.upper = c->upper;
-  a.tight = c->tight;
-  a.mti_seed = 0;
+  DenseArgs a = dense_args(c);
   a.labels_only = 1;
-  a.delta = 0;
-  a.means = c->means;
-  a.chn = c->chn;
-  a.partials = c->partials;
-  a.ctrl = c->ctrl;
-  a.use_tma = c->use_tma;
   KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
   KNB_CUDA(launch_reduce(c->partials, c->G_dense, c->L, c->exch, c->ctrl, c->stream));
   KNB_CUDA(cudaStreamSynchronize(c->stream));  // labels is a caller buffer
@@ -747,8 +759,8 @@ int knb_set_ignore_stop(knb_ctx* c, int32_t on) {
 int knb_set_option(knb_ctx* c, int32_t option, int64_t value) {
   if (!c) return fail(KNB_E_ARG, "null context");
   if (option == KNB_OPT_MTI_SCAN) {
-    if (value < KNB_MTI_AUTO || value > KNB_MTI_DENSE) return fail(KNB_E_ARG, "bad MTI scan mode");
-    if (value == KNB_MTI_DENSE && !c->mti_mma_ok)
+    if (value < KNB_MTI_AUTO || value > KNB_MTI_BLOCK) return fail(KNB_E_ARG, "bad MTI scan mode");
+    if ((value == KNB_MTI_DENSE || value == KNB_MTI_BLOCK) && !c->mti_mma_ok)
       return fail(KNB_E_ARG, "dense MTI scan needs d <= 64 and centroids that fit shared memory");
     c->mti_scan = (int)value;
     return KNB_OK;
@@ -767,7 +779,7 @@ int knb_describe(knb_ctx* c, int32_t* dp, int32_t* tma, int32_t* gd, int32_t* gm
   if (dp) *dp = c->DP;
   if (tma) *tma = c->use_tma;
   if (gd) *gd = c->G_dense;
-  if (gm) *gm = (c->mti_scan != KNB_MTI_EXACT && c->mti_mma_ok) ? -c->G_mti_mma : c->G_mti;
+  if (gm) *gm = (c->mti_scan != KNB_MTI_EXACT && c->mti_mma_ok) ? -c->G_dense : c->G_mti;
   return KNB_OK;
 }
 

@@ -19,6 +19,10 @@ struct DenseArgs {
   int mti_seed;          // 1 on the full pass of a pruned run
   int labels_only;       // accumulate by the labels already in assign (random-partition init)
   int delta;             // dense passes after the first: accumulate signed deltas of moved rows only
+  int mti_filter;        // block-dense MTI pass (clause-1 filter per row, see assign_mma.cu)
+  int gate;              // run only when ctrl->mti_choice == 1
+  const double* drift;   // MTI: per-centroid drift (bound inflation)
+  const double* half_min;
   const double* means;   // k x d
   const double* chn;     // k: -0.5 * ||c_j||^2
   double* partials;      // G x acc_len(k, d)
@@ -38,6 +42,7 @@ struct MtiArgs {
   const double* half;      // k x k
   const double* half_min;  // k
   const double* chn;       // -0.5 ||c||^2 (tensor-core scan)
+  int gate;                // run only when ctrl->mti_choice == 0
   double* partials;
   const Ctrl* ctrl;
   int half_in_smem;

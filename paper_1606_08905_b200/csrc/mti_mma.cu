@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   constexpr int KS = DP / 4;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
+  if (a.gate && a.ctrl->mti_choice != 0) return;  // the block-dense pass runs this iteration
   const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;

@@ -19,6 +19,8 @@ struct Ctrl {
   int ignore_stop;       // bench: keep iterating after convergence (never set by kmeans())
   int max_iters;
   double tolerance;      // reassigned <= tolerance converges
+  int mti_choice;        // next pruned pass: 1 = block-dense (few skips), 0 = compacted survivors
+  int pad_;
   double cmax2;          // max_j ||c_j||^2 of the current means (dense certificate)
   long long count_seen;  // last Sigma counts
 };

@@ -46,14 +46,17 @@ def test_gpu_matches_reference_golden(name):
     assert r.converged == bool(g["converged"])
 
 
+@pytest.mark.parametrize("mode", ["auto", "dense", "block"])
 @pytest.mark.parametrize("name", [n for n in CASES if CASES[n]["cfg"].get("pruning", True)])
-def test_gpu_tensor_core_mti_matches_reference_golden(name):
-    """Default mti_scan ("auto" -> tensor-core survivors): assignments every iteration,
-    centroids, bounds-driven skip counts and reassignments are the reference's; the
-    distance count is k per survivor."""
+def test_gpu_tensor_core_mti_matches_reference_golden(name, mode):
+    """Tensor-core MTI passes (compacted survivors, block-dense, or the device's per-
+    iteration choice): assignments every iteration, centroids, bounds-driven skip counts
+    and reassignments are the reference's; the distance count is k per survivor."""
     g = golden(name)
     m = case_data(name)
-    r = kb.kmeans(m, _cfg(name, collect_assignments=True))
+    if m.shape[1] > 64 and mode != "auto":
+        pytest.skip("tensor-core MTI needs d <= 64")
+    r = kb.kmeans(m, _cfg(name, collect_assignments=True, mti_scan=mode))
     assert_parity(m.astype(np.float64), r, g["means"], g["assignments"], len(g["reassignments"]),
                   want_prev=g["prev_means"], counters={"reassignments": g["reassignments"], "skips": g["skips"]},
                   wcss=g["wcss"], what=name)
