@@ -172,6 +172,13 @@ def run_ours(args):
         host = None
         d = 16
         args.no_e2e = True
+    elif name == "c5":
+        # 10 GB of f32 rows: the mixture law generated in HBM (torch's seeded generator);
+        # the e2e leg copies it to pinned host memory first
+        spec = cfg["spec"](hi - lo)
+        dev_rows = kb.synth.mixture_device(spec, device=local_rank)
+        host = None
+        d = spec.d
     else:
         full = cfg["data"](n)
         host = np.ascontiguousarray(full[lo:hi], dtype=np.float64)
@@ -179,12 +186,15 @@ def run_ours(args):
         dev_rows = torch.from_numpy(host).cuda()
     gen_s = time.perf_counter() - t_gen
     torch.cuda.synchronize()
-    shard_bytes = (hi - lo) * d * 8
+    elem = dev_rows.element_size()
+    shard_bytes = (hi - lo) * d * elem
 
     peaks = load_peaks()
     mp = _native.measure_peaks(local_rank)
     hbm_peak = peaks.get("hbm_gbs") or 6650.0
     dfma_peak = mp["dfma_per_s"]
+    # kind::tf32 runs at half the bf16 rate on sm_100: half the measured cuBLAS bf16 figure
+    tf32_peak = 0.5 * (peaks.get("bf16_tflops") or 2250.0) * 1e12
 
     clocks = Clocks(local_rank)
     total_iters = args.warmup + args.steps + 2
@@ -227,11 +237,17 @@ def run_ours(args):
     # dominant kernel: the local pass (K1 dense or K6/K7 MTI) + its CTA-partial merge
     kern_s = statistics.mean(local_ms) * 1e-3
     n_loc = hi - lo
+    tc = desc["dense_dp"] < 0                        # f32 rows on the tcgen05 path
     flops = 2.0 * n_loc * k * d                      # dense-equivalent (north star definition)
-    bytes_ = 8.0 * n_loc * d                         # point bytes
-    t_fp = flops / (2 * dfma_peak)
+    bytes_ = float(elem) * n_loc * d                 # point bytes
+    fp_peak = tf32_peak if tc else 2 * dfma_peak
+    t_fp = flops / fp_peak
     t_hbm = bytes_ / (hbm_peak * 1e9)
-    if t_fp >= t_hbm:
+    if tc:
+        roof = {"bound": "tensor", "achieved": flops / kern_s / 1e12, "peak": fp_peak / 1e12,
+                "unit": "TFLOP/s", "peak_source": "0.5 x MEASURED_PEAKS.json bf16_tflops (kind::tf32 = half the "
+                                                  "bf16 rate)"}
+    elif t_fp >= t_hbm:
         roof = {"bound": "fp64", "achieved": flops / kern_s / 1e12, "peak": 2 * dfma_peak / 1e12,
                 "unit": "TFLOP/s", "peak_source": "measured in-run DFMA microbenchmark (knb_measure_peaks)"}
     else:
@@ -239,7 +255,8 @@ def run_ours(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
-    roof["kernel"] = "mti_tile_kernel + reduce" if cfg["pruning"] else "dense_tile_kernel + reduce"
+    roof["kernel"] = ("tc_assign_kernel + tc_rerank + segsum" if tc else
+                      "mti_tile_kernel + reduce" if cfg["pruning"] else "dense_tile_kernel + reduce")
     roof["kernel_ms"] = kern_s * 1e3
     roof["work"] = "dense-equivalent 2*n*k*d flops and n*d*8 point bytes per launch; MTI skips are not discounted"
     roof["computed_fraction"] = comps / max(1, n * k * len(timed_stats))
@@ -264,15 +281,17 @@ def run_ours(args):
         torch.cuda.synchronize()
         k1_s = statistics.mean(a.elapsed_time(b) for a, b in kev) * 1e-3
         dense.close()
-        roof_k1 = {"bound": "fp64" if t_fp >= t_hbm else "hbm", "kernel": "dense_tile_kernel + reduce",
+        roof_k1 = {"bound": "tensor" if tc else "fp64" if t_fp >= t_hbm else "hbm",
+                   "kernel": "tc_assign_kernel + tc_rerank + segsum" if tc else "dense_tile_kernel + reduce",
                    "kernel_ms": k1_s * 1e3, "dense_dp": desc["dense_dp"], "tma": desc["tma"]}
-        if t_fp >= t_hbm:
-            roof_k1.update(achieved=flops / k1_s / 1e12, peak=2 * dfma_peak / 1e12, unit="TFLOP/s")
+        if tc or t_fp >= t_hbm:
+            roof_k1.update(achieved=flops / k1_s / 1e12, peak=fp_peak / 1e12, unit="TFLOP/s")
         else:
             roof_k1.update(achieved=bytes_ / k1_s / 1e9, peak=hbm_peak, unit="GB/s")
         roof_k1["frac"] = roof_k1["achieved"] / roof_k1["peak"]
         roof_k1["hbm_GBps"] = bytes_ / k1_s / 1e9
-        roof_k1["fp64_TFLOPs"] = flops / k1_s / 1e12
+        roof_k1["fp64_TFLOPs" if not tc else "tf32_TFLOPs"] = flops / k1_s / 1e12
+    tcinfo = run.ctx.tc_info() if tc else None
     run.close()
 
     # end to end through the public API from host numpy (H2D + init + iterations + D2H)
@@ -280,6 +299,12 @@ def run_ours(args):
     if world == 1 and not args.no_e2e:
         ecfg2 = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"],
                                 max_iters=cfg["max_iters"], tolerance=cfg["tolerance"], device=local_rank)
+        # the user's rows in pinned host memory (H2D at full PCIe/C2C speed)
+        pinned = torch.empty(tuple(dev_rows.shape), dtype=dev_rows.dtype, pin_memory=True)
+        pinned.copy_(dev_rows if host is None else torch.from_numpy(host))
+        host = pinned.numpy()
+        del dev_rows
+        torch.cuda.empty_cache()
         kb.kmeans(host[: min(n, 100_000)], ecfg2)  # warm-up (context + modules)
         vals = []
         for _ in range(args.e2e_reps):
@@ -298,11 +323,14 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         base = cpu_baseline(name, cfg, args.warmup, min(args.steps, 10))
 
-    launches_per_step = 4 + (1 if cfg["pruning"] else 0)
+    # kernels per step: K1/MTI pass + CTA merge + finalize + stats (+ geometry when pruning);
+    # tcgen05 path: prep, assign, rerank, 6 segsum stages, scalars, finalize, stats
+    launches_per_step = 12 if tc else 4 + (1 if cfg["pruning"] else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32 rows: tf32 tensor-core scores + f64 certificate/rerank/sums" if tc else "f64",
+        "data": "synthetic",
         "config": {"workload": name, "n": n, "d": d, "k": k, "init": cfg["init"], "pruning": cfg["pruning"],
                    "tolerance": cfg["tolerance"], "parallelism": f"row-shard x{world}",
                    "l2": f"inputs {shard_bytes / 2**20:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
@@ -312,6 +340,7 @@ def run_ours(args):
         "gpu_launches": launches_per_step * args.steps, "clocks": clk,
         "setup": {"datagen_s": gen_s, "init_s": init_s, "dfma_peak_per_s": dfma_peak,
                   "copy_GBps_measured": mp["copy_bytes_per_s"] / 1e9, "kernels": desc},
+        "tc_certificate": tcinfo,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -66,6 +66,23 @@ int knb_destroy(knb_ctx* ctx);
  * buffer, or attach caller-owned device rows.  Replaces _MemorySource (engine.py:162-191). */
 int knb_upload_rows(knb_ctx* ctx, const double* host, int64_t row_lo_local, int64_t rows);
 int knb_attach_rows(knb_ctx* ctx, const double* dev_rows);
+/* f32 rows (BASELINE config 5), kept as f32 in HBM -- the reference upcasts them to f64
+ * (matrix.py:40), which is exact, and every result here equals the f64 upcast's.  Only the
+ * dense tensor-core path takes them: knb_f32_supported(d, k, pruning) says whether it
+ * applies (pruning off, d % 4 == 0, 32 <= d <= 256); elsewhere the caller upcasts.
+ * Scores come from tcgen05 kind::tf32 with a certified bound; uncertified rows are
+ * re-scored with the exact f64 recipe (distance.py:28-39, :94-116). */
+int knb_f32_supported(int32_t d, int32_t k, int32_t pruning);
+int knb_upload_rows_f32(knb_ctx* ctx, const float* host, int64_t row_lo_local, int64_t rows);
+int knb_attach_rows_f32(knb_ctx* ctx, const float* dev_rows);
+/* Tensor-core path counters since the last centroid install: rows whose certificate
+ * failed (re-scored exactly) and, of those, rows re-scored against all k. */
+int knb_tc_info(knb_ctx* ctx, int32_t* active, int64_t* flagged_rows, int64_t* full_reranks);
+/* Diagnostics of the certificate: the tensor-core scores x.c_j - ||c_j||^2/2 (f32) of every
+ * shard row against the current centroids into dev_out (n_local x k_pad, k rounded up to
+ * 256; padding scores are -inf), and the relative error e the certificate assumes
+ * (|score error| <= e ||x|| max_j ||c_j|| + rounding terms).  Assignments are untouched. */
+int knb_tc_scores(knb_ctx* ctx, float* dev_out, double* err_rel);
 /* check_matrix's finite scan (matrix.py:46-48): *first_bad = first shard-local row with a
  * NaN/inf, or -1. */
 int knb_check_finite(knb_ctx* ctx, int64_t* first_bad);
@@ -142,8 +159,9 @@ int knb_set_ignore_stop(knb_ctx* ctx, int32_t on);
 int knb_set_option(knb_ctx* ctx, int32_t option, int64_t value);
 /* Device bytes held by the context (the GPU analogue of KmeansResult.peak_state_bytes). */
 int knb_state_bytes(knb_ctx* ctx, int64_t* bytes);
-/* Which kernels the context uses: padded width (0 = generic), TMA on/off, grid sizes
- * (grid_mti < 0: the tensor-core MTI kernel with -grid_mti CTAs). */
+/* Which kernels the context uses: padded width (0 = generic, < 0: f32 rows on the tcgen05
+ * path with that padded width), TMA on/off, grid sizes (grid_mti < 0: the tensor-core MTI
+ * kernel with -grid_mti CTAs). */
 int knb_describe(knb_ctx* ctx, int32_t* dense_dp, int32_t* use_tma, int32_t* grid_dense, int32_t* grid_mti);
 
 /* numpy's default_rng(seed).random(...) on the device: writes draws [first_draw,

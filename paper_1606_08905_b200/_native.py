@@ -55,6 +55,10 @@ SIGNATURES = {
     "knb_destroy": [_P],
     "knb_upload_rows": [_P, _P, _I64, _I64],
     "knb_attach_rows": [_P, _P],
+    "knb_upload_rows_f32": [_P, _P, _I64, _I64],
+    "knb_attach_rows_f32": [_P, _P],
+    "knb_tc_info": [_P, _PI32, _PI64, _PI64],
+    "knb_tc_scores": [_P, _P, _PD],
     "knb_check_finite": [_P, _PI64],
     "knb_exchange_len": [_P, _PI64],
     "knb_set_exchange": [_P, _P, _I64],
@@ -107,6 +111,8 @@ def lib():
     h.knb_version.argtypes = []
     h.knb_last_error.restype = ctypes.c_char_p
     h.knb_last_error.argtypes = []
+    h.knb_f32_supported.restype = ctypes.c_int
+    h.knb_f32_supported.argtypes = [_I32, _I32, _I32]
     for name, args in SIGNATURES.items():
         fn = getattr(h, name)
         fn.restype = ctypes.c_int
@@ -174,6 +180,31 @@ class Context:
 
     def attach(self, dev_ptr: int) -> None:
         check(self.L.knb_attach_rows(self.h, ctypes.c_void_p(dev_ptr)))
+
+    def upload_f32(self, rows: np.ndarray, lo: int = 0) -> None:
+        """f32 rows for the tensor-core path (see f32_supported)."""
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        check(self.L.knb_upload_rows_f32(self.h, ptr(rows), lo, rows.shape[0]))
+        self.sync()
+
+    def upload_f32_async(self, rows: np.ndarray, lo: int = 0) -> None:
+        check(self.L.knb_upload_rows_f32(self.h, ptr(rows), lo, rows.shape[0]))
+
+    def attach_f32(self, dev_ptr: int) -> None:
+        check(self.L.knb_attach_rows_f32(self.h, ctypes.c_void_p(dev_ptr)))
+
+    def tc_scores(self, dev_ptr: int) -> float:
+        """Dump the tensor-core scores (n_local x k_pad f32) into device memory at
+        ``dev_ptr``; returns the certificate's relative error e."""
+        e = ctypes.c_double()
+        check(self.L.knb_tc_scores(self.h, ctypes.c_void_p(dev_ptr), ctypes.byref(e)))
+        return float(e.value)
+
+    def tc_info(self) -> dict:
+        a = ctypes.c_int32()
+        f, g = ctypes.c_int64(), ctypes.c_int64()
+        check(self.L.knb_tc_info(self.h, ctypes.byref(a), ctypes.byref(f), ctypes.byref(g)))
+        return dict(active=bool(a.value), flagged_rows=int(f.value), full_reranks=int(g.value))
 
     def first_nonfinite_row(self) -> int:
         v = ctypes.c_int64()
@@ -302,6 +333,11 @@ class Context:
         check(self.L.knb_describe(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
         return dict(dense_dp=a.value, tma=bool(b.value), grid_dense=c.value,
                     grid_mti=abs(d.value), mti_kernel="tensor-core" if d.value < 0 else "exact-scan")
+
+
+def f32_supported(d: int, k: int, pruning: bool) -> bool:
+    """Whether f32 rows stay f32 on the device (dense tcgen05 path); else they are upcast."""
+    return bool(lib().knb_f32_supported(int(d), int(k), int(bool(pruning))))
 
 
 def device_info(device: int = 0) -> dict:

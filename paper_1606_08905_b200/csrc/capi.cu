@@ -35,6 +35,8 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr size_t SMEM_LIMIT = 227 * 1024;
+// certified relative error of one kind::tf32 dot product (assign_tc.cu header)
+constexpr double KNB_TF32_ERR = 0x1p-8;
 
 }  // namespace
 
@@ -52,6 +54,25 @@ struct knb_ctx {
   CUtensorMap tmap;
   int use_tma = 0;
 
+  // f32 rows on the tcgen05 path (assign_tc.cu + segsum.cu)
+  int elem = 8;
+  const float* X32 = nullptr;
+  float* X32_own = nullptr;
+  bool tc = false;
+  CUtensorMap tmX32, tmC32;
+  int kp = 0, dp = 0, nkc = 0, nnt = 0, G_tc = 1;
+  float *c32 = nullptr, *chn32 = nullptr;
+  double* xn2 = nullptr;
+  bool xn_valid = false;
+  int32_t* old_assign = nullptr;
+  float* tc_bound = nullptr;
+  TcHalf* tc_scratch = nullptr;
+  int4* tcq = nullptr;
+  int* tcq_count = nullptr;
+  long long tcq_cap = 0;
+  unsigned long long* tc_counters = nullptr;
+  SegArgs seg;
+
   int DP = 0, DPm = 0, half_in_smem = 0;
   int G_dense = 1, G_mti = 1, G_mti_mma = 1;
   int mti_scan = 0;   // KNB_MTI_AUTO / KNB_MTI_EXACT / KNB_MTI_DENSE
@@ -66,7 +87,7 @@ struct knb_ctx {
   double* exch = nullptr;
   bool own_exch = true;
   long long L = 0;
-  double* partials = nullptr;
+  double* partials = nullptr;  // allocated on first use by an f64 pass
   int G_alloc = 0;
   Ctrl* ctrl = nullptr;
   IterStatsDev* stats = nullptr;
@@ -114,6 +135,7 @@ FinalArgs final_args(knb_ctx* c) {
   f.half = c->half;
   f.half_min = c->half_min;
   f.wterm = c->wterm;
+  f.wcss_mode = c->tc ? 2 : (c->pruning ? 1 : 0);
   f.ctrl = c->ctrl;
   f.stats = c->stats;
   return f;
@@ -129,6 +151,7 @@ int reset_run(knb_ctx* c) {
   KNB_CUDA(cudaMemcpyAsync(c->ctrl, &h, offsetof(Ctrl, cmax2), cudaMemcpyHostToDevice, c->stream));
   KNB_CUDA(cudaMemsetAsync(c->assign, 0, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
   KNB_CUDA(cudaMemsetAsync(c->run, 0, sizeof(double) * c->L, c->stream));
+  if (c->tc_counters) KNB_CUDA(cudaMemsetAsync(c->tc_counters, 0, 4 * sizeof(unsigned long long), c->stream));
   c->t_host = 0;
   return KNB_OK;
 }
@@ -166,11 +189,181 @@ int build_tmap(knb_ctx* c) {
 
 int need_ready(knb_ctx* c, bool centroids) {
   if (!c) return fail(KNB_E_ARG, "null context");
-  if (!c->X && c->n_local > 0) return fail(KNB_E_STATE, "rows not uploaded or attached");
+  if (!c->X && !c->X32 && c->n_local > 0) return fail(KNB_E_STATE, "rows not uploaded or attached");
   if (centroids && !c->centroids_set) return fail(KNB_E_STATE, "centroids not initialised");
   cudaError_t e = cudaSetDevice(c->device);
   if (e != cudaSuccess) return fail(KNB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
   return KNB_OK;
+}
+
+const void* rows_of(const knb_ctx* c) {
+  return c->elem == 4 ? static_cast<const void*>(c->X32) : static_cast<const void*>(c->X);
+}
+
+int ensure_partials(knb_ctx* c) {
+  if (c->partials) return KNB_OK;
+  return dev_alloc(c, &c->partials, (size_t)c->G_alloc * c->L);
+}
+
+bool f32_supported(int d, int k, int pruning) {
+  return !pruning && d % 4 == 0 && d >= 32 && d <= 256 && k >= 1 && k <= 16384;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+// 2-D f32 map, 32-column (128 B) boxes with the 128-byte swizzle the UMMA
+// descriptors expect; columns past `cols` read as zeros.
+int encode_f32_map(CUtensorMap* m, const float* p, long long cols, long long rows, int box_rows) {
+  auto encode = tensor_map_encoder();
+  if (!encode) return fail(KNB_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old for the f32 path)");
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), gdim, gstride, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KNB_E_CUDA, "cuTensorMapEncodeTiled failed for f32 rows (" + std::to_string((int)r) + ")");
+  return KNB_OK;
+}
+
+// first f32 rows: switch the context to the tensor-core path and allocate its state
+int tc_setup(knb_ctx* c) {
+  if (c->tc) return KNB_OK;
+  if (!f32_supported(c->d, c->k, c->pruning))
+    return fail(KNB_E_ARG, "f32 rows need the dense tensor-core path: pruning off, d % 4 == 0, 32 <= d <= 256, k <= 16384");
+  if (c->n_local > (1LL << 30)) return fail(KNB_E_ARG, "f32 path: at most 2^30 rows per GPU");
+  if (c->X) return fail(KNB_E_STATE, "context already holds f64 rows");
+  const long long nl = c->n_local ? c->n_local : 1;
+  c->elem = 4;
+  c->kp = (c->k + 255) / 256 * 256;
+  c->dp = (c->d + 31) / 32 * 32;
+  c->nkc = c->dp / 32;
+  c->nnt = c->kp / 256;
+  const long long tiles = (nl + tc_rows_per_tile() - 1) / tc_rows_per_tile();
+  c->G_tc = (int)(tiles < c->sms ? tiles : c->sms);
+  c->tcq_cap = (tiles + c->G_tc - 1) / c->G_tc * 32;
+  int rc;
+  if ((rc = dev_alloc(c, &c->c32, (size_t)c->kp * c->dp))) return rc;
+  if ((rc = dev_alloc(c, &c->chn32, c->kp))) return rc;
+  if ((rc = dev_alloc(c, &c->xn2, nl))) return rc;
+  if ((rc = dev_alloc(c, &c->old_assign, nl))) return rc;
+  if ((rc = dev_alloc(c, &c->tc_bound, nl))) return rc;
+  if ((rc = dev_alloc(c, &c->tc_scratch, (size_t)c->G_tc * 2 * tc_rows_per_tile()))) return rc;
+  if ((rc = dev_alloc(c, &c->tcq, (size_t)c->G_tc * 4 * 2 * c->tcq_cap))) return rc;
+  if ((rc = dev_alloc(c, &c->tcq_count, (size_t)c->G_tc * 4))) return rc;
+  if ((rc = dev_alloc(c, &c->tc_counters, 4))) return rc;
+  KNB_CUDA(cudaMemsetAsync(c->tc_counters, 0, 4 * sizeof(unsigned long long), c->stream));
+  KNB_CUDA(cudaMemsetAsync(c->tcq_count, 0, sizeof(int) * c->G_tc * 4, c->stream));
+  KNB_CUDA(cudaMemsetAsync(c->c32, 0, sizeof(float) * (size_t)c->kp * c->dp, c->stream));
+  if ((rc = encode_f32_map(&c->tmC32, c->c32, c->dp, c->kp, 256))) return rc;
+  // cluster-sorted accumulation
+  SegArgs& g = c->seg;
+  std::memset(&g, 0, sizeof(g));
+  g.n = c->n_local;
+  g.d = c->d;
+  g.k = c->k;
+  g.B = seg_blocks(nl);
+  if ((rc = dev_alloc(c, &g.counts, (size_t)c->k * g.B))) return rc;
+  if ((rc = dev_alloc(c, &g.lrank, 2 * (size_t)nl))) return rc;
+  if ((rc = dev_alloc(c, &g.ctot, c->k))) return rc;
+  if ((rc = dev_alloc(c, &g.cstart, c->k + 1))) return rc;
+  if ((rc = dev_alloc(c, &g.istart, c->k + 1))) return rc;
+  if ((rc = dev_alloc(c, &g.sorted, 2 * (size_t)nl))) return rc;
+  if ((rc = dev_alloc(c, &g.records, (size_t)seg_max_items(nl, c->k) * (c->d + 2)))) return rc;
+  c->tc = true;
+  return KNB_OK;
+}
+
+int tc_attach(knb_ctx* c, const float* p) {
+  c->X32 = p;
+  c->xn_valid = false;
+  if (reinterpret_cast<uintptr_t>(p) & 15) return fail(KNB_E_ARG, "f32 rows must be 16-byte aligned");
+  if (c->n_local > 0) return encode_f32_map(&c->tmX32, p, c->d, c->n_local, tc_rows_per_tile());
+  return KNB_OK;
+}
+
+SegArgs seg_args(knb_ctx* c, int mode, const int32_t* labels) {
+  SegArgs g = c->seg;
+  g.X = rows_of(c);
+  g.assign = labels;
+  g.old_assign = c->old_assign;
+  g.xn2 = c->xn2;
+  g.mode = mode;
+  g.exch = c->exch;
+  g.ctrl = c->ctrl;
+  return g;
+}
+
+int ensure_xn2(knb_ctx* c) {
+  if (c->xn_valid) return KNB_OK;
+  if (c->n_local) KNB_CUDA(launch_row_sqnorm_f32(c->X32, c->n_local, c->d, c->xn2, c->stream));
+  c->xn_valid = true;
+  return KNB_OK;
+}
+
+TcArgs tc_args(knb_ctx* c);
+
+// one dense pass of f32 rows: TF32 scores + certificate, exact rerank of the
+// uncertified rows, cluster-sorted accumulation (full on the first pass, signed
+// deltas of the moved rows afterwards), scalars
+int tc_local(knb_ctx* c) {
+  int rc = ensure_xn2(c);
+  if (rc) return rc;
+  KNB_CUDA(cudaMemsetAsync(c->tc_counters, 0, sizeof(unsigned long long), c->stream));
+  KNB_CUDA(launch_tc_prep(c->means, c->cn2, c->k, c->d, c->kp, c->dp, c->c32, c->chn32, c->stream));
+  TcArgs a = tc_args(c);
+  if (c->n_local) {
+    if (c->t_host == 0) {
+      // no distance bounds yet: one scoring pass for each row's maximum, then the
+      // collecting pass with the exact window
+      a.mode = TC_MAX;
+      KNB_CUDA(launch_tc_assign(&c->tmX32, &c->tmC32, a, c->G_tc, c->stream));
+      a.mode = TC_COLLECT_SMAX;
+    }
+    KNB_CUDA(launch_tc_assign(&c->tmX32, &c->tmC32, a, c->G_tc, c->stream));
+    KNB_CUDA(launch_tc_rerank(a, c->means, c->G_tc * 4, c->stream));
+  }
+  SegArgs g = seg_args(c, c->t_host == 0 ? 0 : 1, c->assign);
+  KNB_CUDA(launch_segsum(g, 4, c->stream));
+  KNB_CUDA(launch_tc_scalars(c->tc_counters, c->n_local, c->k, c->d, c->exch, c->ctrl, c->stream));
+  return KNB_OK;
+}
+
+TcArgs tc_args(knb_ctx* c) {
+  TcArgs a;
+  a.X = c->X32;
+  a.n = c->n_local;
+  a.d = c->d;
+  a.k = c->k;
+  a.kp = c->kp;
+  a.nkc = c->nkc;
+  a.nnt = c->nnt;
+  a.assign = c->assign;
+  a.old_assign = c->old_assign;
+  a.xn2 = c->xn2;
+  a.chn32 = c->chn32;
+  a.queue = c->tcq;
+  a.qcount = c->tcq_count;
+  a.qcap = c->tcq_cap;
+  a.counters = c->tc_counters;
+  a.ctrl = c->ctrl;
+  a.err_rel = KNB_TF32_ERR;
+  a.dbg = nullptr;
+  a.mode = TC_COLLECT_BOUND;
+  a.bound = c->tc_bound;
+  a.drift = c->drift;
+  a.scratch = c->tc_scratch;
+  return a;
 }
 
 DenseArgs dense_args(knb_ctx* c) {
@@ -198,6 +391,9 @@ DenseArgs dense_args(knb_ctx* c) {
 }
 
 int launch_local(knb_ctx* c) {
+  if (c->tc) return tc_local(c);
+  int rc = ensure_partials(c);
+  if (rc) return rc;
   const bool full = !c->pruning || c->t_host == 0;
   if (full) {
     DenseArgs a = dense_args(c);
@@ -309,6 +505,9 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   KNB_CUDA(cudaSetDevice(device));
   knb_ctx* c = new knb_ctx();
   std::memset(&c->tmap, 0, sizeof(c->tmap));
+  std::memset(&c->tmX32, 0, sizeof(c->tmX32));
+  std::memset(&c->tmC32, 0, sizeof(c->tmC32));
+  std::memset(&c->seg, 0, sizeof(c->seg));
   c->device = device;
   c->n_global = n_global;
   c->n_local = n_local;
@@ -382,7 +581,6 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   if ((rc = dev_alloc(c, &c->cn2, k))) return bail(rc);
   if ((rc = dev_alloc(c, &c->wterm, k))) return bail(rc);
   if ((rc = dev_alloc(c, &c->exch, c->L))) return bail(rc);
-  if ((rc = dev_alloc(c, &c->partials, (size_t)c->G_alloc * c->L))) return bail(rc);
   if ((rc = dev_alloc(c, &c->ctrl, 1))) return bail(rc);
   if ((rc = dev_alloc(c, &c->stats, max_iters))) return bail(rc);
   if ((rc = dev_alloc(c, &c->bad, 2))) return bail(rc);
@@ -400,7 +598,9 @@ int knb_destroy(knb_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
                   c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->stats,
-                  c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx};
+                  c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
+                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tcq, c->tcq_count, c->tc_counters, c->seg.counts,
+                  c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (c->own_exch && c->exch) cudaFree(c->exch);
@@ -409,8 +609,66 @@ int knb_destroy(knb_ctx* c) {
   return KNB_OK;
 }
 
+int knb_f32_supported(int32_t d, int32_t k, int32_t pruning) { return f32_supported(d, k, pruning) ? 1 : 0; }
+
+int knb_upload_rows_f32(knb_ctx* c, const float* host, int64_t lo, int64_t rows) {
+  if (!c || (!host && rows > 0)) return fail(KNB_E_ARG, "null argument");
+  if (lo < 0 || rows < 0 || lo + rows > c->n_local) return fail(KNB_E_ARG, "row range outside the shard");
+  KNB_CUDA(cudaSetDevice(c->device));
+  int rc;
+  if (!c->X32_own) {
+    if ((rc = tc_setup(c))) return rc;
+    if ((rc = dev_alloc(c, &c->X32_own, (size_t)(c->n_local ? c->n_local : 1) * c->d))) return rc;
+    if ((rc = tc_attach(c, c->X32_own))) return rc;
+  }
+  c->xn_valid = false;
+  if (rows)
+    KNB_CUDA(cudaMemcpyAsync(c->X32_own + lo * c->d, host, sizeof(float) * rows * c->d, cudaMemcpyHostToDevice,
+                             c->stream));
+  return KNB_OK;
+}
+
+int knb_attach_rows_f32(knb_ctx* c, const float* dev) {
+  if (!c || !dev) return fail(KNB_E_ARG, "null argument");
+  KNB_CUDA(cudaSetDevice(c->device));
+  int rc = tc_setup(c);
+  if (rc) return rc;
+  return tc_attach(c, dev);
+}
+
+int knb_tc_info(knb_ctx* c, int32_t* active, int64_t* flagged, int64_t* full_reranks) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (active) *active = c->tc ? 1 : 0;
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (c->tc) {
+    KNB_CUDA(cudaSetDevice(c->device));
+    KNB_CUDA(cudaMemcpyAsync(h, c->tc_counters, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (flagged) *flagged = (int64_t)h[1];
+  if (full_reranks) *full_reranks = (int64_t)h[2];
+  return KNB_OK;
+}
+
+int knb_tc_scores(knb_ctx* c, float* dev_out, double* err_rel) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  if (!c->tc) return fail(KNB_E_STATE, "no f32 rows on the tensor-core path");
+  if (!dev_out) return fail(KNB_E_ARG, "null output");
+  if ((rc = ensure_xn2(c))) return rc;
+  KNB_CUDA(launch_tc_prep(c->means, c->cn2, c->k, c->d, c->kp, c->dp, c->c32, c->chn32, c->stream));
+  TcArgs a = tc_args(c);
+  a.dbg = dev_out;
+  a.mode = TC_MAX;
+  if (c->n_local) KNB_CUDA(launch_tc_assign(&c->tmX32, &c->tmC32, a, c->G_tc, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (err_rel) *err_rel = KNB_TF32_ERR;
+  return KNB_OK;
+}
+
 int knb_upload_rows(knb_ctx* c, const double* host, int64_t lo, int64_t rows) {
   if (!c || (!host && rows > 0)) return fail(KNB_E_ARG, "null argument");
+  if (c->tc) return fail(KNB_E_STATE, "context holds f32 rows");
   if (lo < 0 || rows < 0 || lo + rows > c->n_local) return fail(KNB_E_ARG, "row range outside the shard");
   KNB_CUDA(cudaSetDevice(c->device));
   if (!c->X_own) {
@@ -428,6 +686,7 @@ int knb_upload_rows(knb_ctx* c, const double* host, int64_t lo, int64_t rows) {
 
 int knb_attach_rows(knb_ctx* c, const double* dev) {
   if (!c || !dev) return fail(KNB_E_ARG, "null argument");
+  if (c->tc) return fail(KNB_E_STATE, "context holds f32 rows");
   KNB_CUDA(cudaSetDevice(c->device));
   c->X = dev;
   return build_tmap(c);
@@ -437,7 +696,7 @@ int knb_check_finite(knb_ctx* c, int64_t* first_bad) {
   int rc = need_ready(c, false);
   if (rc) return rc;
   KNB_CUDA(cudaMemsetAsync(c->bad, 0xff, sizeof(long long), c->stream));
-  if (c->n_local) KNB_CUDA(launch_check_finite(c->X, c->n_local, c->d, c->bad, c->stream));
+  if (c->n_local) KNB_CUDA(launch_check_finite(rows_of(c), c->elem, c->n_local, c->d, c->bad, c->stream));
   long long h;
   KNB_CUDA(cudaMemcpyAsync(&h, c->bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   KNB_CUDA(cudaStreamSynchronize(c->stream));
@@ -494,7 +753,8 @@ int knb_init_gather(knb_ctx* c, const int64_t* ids, int32_t count) {
   KNB_CUDA(cudaMemcpyAsync(c->ids_dev, ids, sizeof(long long) * count, cudaMemcpyHostToDevice, c->stream));
   KNB_CUDA(cudaMemsetAsync(c->exch, 0, sizeof(double) * count * c->d, c->stream));
   if (c->n_local)
-    KNB_CUDA(launch_gather_rows(c->X, c->n_local, c->row_lo, c->d, c->ids_dev, count, c->exch, c->stream));
+    KNB_CUDA(launch_gather_rows(rows_of(c), c->elem, c->n_local, c->row_lo, c->d, c->ids_dev, count, c->exch,
+                                c->stream));
   KNB_CUDA(cudaStreamSynchronize(c->stream));  // ids is a caller buffer
   return KNB_OK;
 }
@@ -521,6 +781,13 @@ int knb_init_partition_local(knb_ctx* c, const int32_t* labels) {
   if (rc) return rc;
   if (c->n_local)
     KNB_CUDA(cudaMemcpyAsync(c->assign, labels, sizeof(int32_t) * c->n_local, cudaMemcpyHostToDevice, c->stream));
+  if (c->tc) {
+    if ((rc = ensure_xn2(c))) return rc;
+    KNB_CUDA(launch_segsum(seg_args(c, 0, c->assign), 4, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));  // labels is a caller buffer
+    return KNB_OK;
+  }
+  if ((rc = ensure_partials(c))) return rc;
   DenseArgs a = dense_args(c);
   a.labels_only = 1;
   KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
@@ -556,7 +823,8 @@ int knb_kpp_update(knb_ctx* c, int32_t first, double* local_total) {
   if ((rc = kpp_buffers(c))) return rc;
   double h = 0.0;
   if (c->n_local) {
-    KNB_CUDA(launch_kpp_update(c->X, c->n_local, c->d, c->exch, c->d2, first, c->kpp_bs, c->kpp_nblk, c->stream));
+    KNB_CUDA(launch_kpp_update(rows_of(c), c->elem, c->n_local, c->d, c->exch, c->d2, first, c->kpp_bs,
+                               c->kpp_nblk, c->stream));
     KNB_CUDA(launch_sum_blocks(c->kpp_bs, c->kpp_nblk, c->kpp_scalar, c->stream));
     KNB_CUDA(cudaMemcpyAsync(&h, c->kpp_scalar, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     KNB_CUDA(cudaStreamSynchronize(c->stream));
@@ -776,7 +1044,7 @@ int knb_state_bytes(knb_ctx* c, int64_t* bytes) {
 
 int knb_describe(knb_ctx* c, int32_t* dp, int32_t* tma, int32_t* gd, int32_t* gm) {
   if (!c) return fail(KNB_E_ARG, "null context");
-  if (dp) *dp = c->DP;
+  if (dp) *dp = c->tc ? -c->dp : c->DP;  // negative: f32 rows on the tcgen05 path
   if (tma) *tma = c->use_tma;
   if (gd) *gd = c->G_dense;
   if (gm) *gm = (c->mti_scan != KNB_MTI_EXACT && c->mti_mma_ok) ? -c->G_dense : c->G_mti;

@@ -84,8 +84,9 @@ __device__ __forceinline__ double exact_sq(const XS& x, const CS& c, int d) {
 }
 
 // Runtime-d variant for arbitrary d (no register array): same tree.
-__device__ __forceinline__ double exact_sq_rt(const double* __restrict__ x,
-                                             const double* __restrict__ c, int d) {
+// TX = double, or float for f32 rows (the reference's f64 upcast is exact).
+template <typename TX>
+__device__ __forceinline__ double exact_sq_rt(const TX* __restrict__ x, const double* __restrict__ c, int d) {
   const int n1 = d & ~15, n32 = n1 & ~31;
   double dot = 0.0;
   if (n1) {
@@ -99,7 +100,7 @@ __device__ __forceinline__ double exact_sq_rt(const double* __restrict__ x,
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
-          double v = __dsub_rn(x[i + 8 * a + l], c[i + 8 * a + l]);
+          double v = __dsub_rn((double)x[i + 8 * a + l], c[i + 8 * a + l]);
           z[a][l] = __fma_rn(v, v, z[a][l]);
         }
     }
@@ -113,7 +114,7 @@ __device__ __forceinline__ double exact_sq_rt(const double* __restrict__ x,
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-          double v = __dsub_rn(x[i + 4 * a + l], c[i + 4 * a + l]);
+          double v = __dsub_rn((double)x[i + 4 * a + l], c[i + 4 * a + l]);
           acc[a][l] = __fma_rn(v, v, acc[a][l]);
         }
     }
@@ -124,7 +125,7 @@ __device__ __forceinline__ double exact_sq_rt(const double* __restrict__ x,
     dot = __dadd_rn(__dadd_rn(s[0], s[2]), __dadd_rn(s[1], s[3]));
   }
   for (int i = n1; i < d; ++i) {
-    double v = __dsub_rn(x[i], c[i]);
+    double v = __dsub_rn((double)x[i], c[i]);
     dot = __fma_rn(v, v, dot);
   }
   return dot;

@@ -24,19 +24,21 @@ namespace knb {
 
 namespace {
 
-__global__ void gather_rows_kernel(const double* __restrict__ X, long long n_local, long long row_lo,
+template <typename T>
+__global__ void gather_rows_kernel(const T* __restrict__ X, long long n_local, long long row_lo,
                                    int d, const long long* __restrict__ ids, int count,
                                    double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)count * d;
        i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / d), e = (int)(i - (long long)r * d);
     const long long g = ids[r] - row_lo;
-    if (g >= 0 && g < n_local) out[i] = X[g * d + e];
+    if (g >= 0 && g < n_local) out[i] = (double)X[g * d + e];
   }
 }
 
 // d2 update + per-block (KPP_BLOCK rows) sums of d2, fixed order inside a block
-__global__ void kpp_update_kernel(const double* __restrict__ X, long long n, int d,
+template <typename T>
+__global__ void kpp_update_kernel(const T* __restrict__ X, long long n, int d,
                                   const double* __restrict__ c, double* __restrict__ d2, int first,
                                   double* __restrict__ block_sums) {
   __shared__ double sh[32];
@@ -162,7 +164,8 @@ __global__ void validate_kernel(const double* __restrict__ X, long long n, int d
   }
 }
 
-__global__ void check_finite_kernel(const double* __restrict__ X, long long total, int d, long long* first_bad) {
+template <typename T>
+__global__ void check_finite_kernel(const T* __restrict__ X, long long total, int d, long long* first_bad) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     if (!isfinite(X[i])) atomicMin(reinterpret_cast<unsigned long long*>(first_bad), (unsigned long long)(i / d));
@@ -171,19 +174,25 @@ __global__ void check_finite_kernel(const double* __restrict__ X, long long tota
 
 }  // namespace
 
-cudaError_t launch_gather_rows(const double* X, long long n_local, long long row_lo, int d,
+cudaError_t launch_gather_rows(const void* X, int elem, long long n_local, long long row_lo, int d,
                                const long long* ids, int count, double* out, cudaStream_t s) {
   long long tot = (long long)count * d;
   int blocks = (int)((tot + 255) / 256);
   if (blocks < 1) blocks = 1;
   if (blocks > 4096) blocks = 4096;
-  gather_rows_kernel<<<blocks, 256, 0, s>>>(X, n_local, row_lo, d, ids, count, out);
+  if (elem == 4)
+    gather_rows_kernel<<<blocks, 256, 0, s>>>(static_cast<const float*>(X), n_local, row_lo, d, ids, count, out);
+  else
+    gather_rows_kernel<<<blocks, 256, 0, s>>>(static_cast<const double*>(X), n_local, row_lo, d, ids, count, out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_kpp_update(const double* X, long long n, int d, const double* c, double* d2, int first,
+cudaError_t launch_kpp_update(const void* X, int elem, long long n, int d, const double* c, double* d2, int first,
                               double* block_sums, int nblk, cudaStream_t s) {
-  kpp_update_kernel<<<nblk, 256, 0, s>>>(X, n, d, c, d2, first, block_sums);
+  if (elem == 4)
+    kpp_update_kernel<<<nblk, 256, 0, s>>>(static_cast<const float*>(X), n, d, c, d2, first, block_sums);
+  else
+    kpp_update_kernel<<<nblk, 256, 0, s>>>(static_cast<const double*>(X), n, d, c, d2, first, block_sums);
   return cudaGetLastError();
 }
 
@@ -210,8 +219,11 @@ cudaError_t launch_validate(const double* X, long long n, int d, int k, const in
   return cudaGetLastError();
 }
 
-cudaError_t launch_check_finite(const double* X, long long n, int d, long long* first_bad, cudaStream_t s) {
-  check_finite_kernel<<<1184, 256, 0, s>>>(X, n * d, d, first_bad);
+cudaError_t launch_check_finite(const void* X, int elem, long long n, int d, long long* first_bad, cudaStream_t s) {
+  if (elem == 4)
+    check_finite_kernel<<<1184, 256, 0, s>>>(static_cast<const float*>(X), n * d, d, first_bad);
+  else
+    check_finite_kernel<<<1184, 256, 0, s>>>(static_cast<const double*>(X), n * d, d, first_bad);
   return cudaGetLastError();
 }
 

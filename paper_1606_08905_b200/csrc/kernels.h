@@ -63,9 +63,74 @@ struct FinalArgs {
   double* half;
   double* half_min;
   double* wterm;         // k: per-centroid WCSS terms (pruned runs)
+  int wcss_mode;         // 0: K1's scalar, 1: pruned formula, 2: dense from running sums
   Ctrl* ctrl;
   IterStatsDev* stats;   // [max_iters]
 };
+
+// f32 rows on the tcgen05 tensor cores (assign_tc.cu)
+struct TcHalf {          // one row's window result from the second epilogue half
+  float best, dropped;
+  float v[8];            // its TOPK largest window scores, descending
+  int j[8];
+};
+struct TcArgs {
+  const float* X;        // n x d row-major f32 (shard-local rows)
+  long long n;
+  int d, k;
+  int kp, nkc, nnt;      // centroids padded to 256s; 32-column K chunks; 256-column N tiles
+  int32_t* assign;
+  int32_t* old_assign;   // assignment before this pass (delta accumulation)
+  const double* xn2;     // ||x||^2 per row
+  const float* chn32;    // -||c||^2 / 2 per padded centroid (-inf padding)
+  int4* queue;           // rerank entries (2 x int4: row + up to 7 candidates), qcap per epilogue warp
+  int* qcount;           // entries per epilogue warp
+  long long qcap;
+  unsigned long long* counters;  // [0] reassigned this pass, [1] flagged rows, [2] full reranks (cumulative)
+  const Ctrl* ctrl;
+  double err_rel;        // certified relative error of a TF32 dot product
+  float* dbg;            // non-null: dump the n x kp f32 scores instead of assigning
+  int mode;              // TC_MAX / TC_COLLECT_SMAX / TC_COLLECT_BOUND
+  float* bound;          // per row: max score (TC_MAX out) or distance upper bound (in/out)
+  const double* drift;   // per centroid: distance moved by the last finalize
+  TcHalf* scratch;       // [grid][2][128] hand-over between the epilogue halves
+};
+enum TcMode { TC_MAX = 0, TC_COLLECT_SMAX = 1, TC_COLLECT_BOUND = 2 };
+size_t tc_smem_bytes(int nkc);
+int tc_rows_per_tile();
+int tc_cols_per_tile();
+cudaError_t launch_tc_assign(const CUtensorMap* tmX, const CUtensorMap* tmC, const TcArgs& a, int grid,
+                             cudaStream_t s);
+cudaError_t launch_tc_rerank(const TcArgs& a, const double* means, int regions, cudaStream_t s);
+cudaError_t launch_tc_prep(const double* means, const double* cn2, int k, int d, int kp, int dp, float* c32,
+                           float* chn32, cudaStream_t s);
+cudaError_t launch_row_sqnorm_f32(const float* X, long long n, int d, double* out, cudaStream_t s);
+cudaError_t launch_tc_scalars(const unsigned long long* counters, long long n_local, int k, int d,
+                              double* exch, const Ctrl* ctrl, cudaStream_t s);
+
+// deterministic cluster-sorted accumulation (segsum.cu)
+struct SegArgs {
+  const void* X;         // f32 or f64 rows
+  long long n;
+  int d, k;
+  const int32_t* assign;      // new labels
+  const int32_t* old_assign;  // mode 1: labels before the pass
+  const double* xn2;          // per-row ||x||^2 for the sq slot (or null)
+  int mode;                   // 0: every row +x to assign; 1: moved rows +x new, -x old
+  int B;                      // local blocks
+  int* counts;                // [k][B]
+  int* lrank;                 // [2n]
+  int* ctot;                  // [k]
+  int* cstart;                // [k + 1]
+  int* istart;                // [k + 1]
+  long long* sorted;          // [2n]
+  double* records;            // [items][d + 2]
+  double* exch;               // out: sums, counts, sq
+  const Ctrl* ctrl;
+};
+int seg_blocks(long long n);
+long long seg_max_items(long long n, int k);
+cudaError_t launch_segsum(const SegArgs& a, int elem, cudaStream_t s);
 
 // kernel selection helpers
 int dense_mma_dp(int d);
@@ -90,9 +155,10 @@ cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t s);
 cudaError_t launch_geometry(const FinalArgs& f, cudaStream_t s);
 
 // init helpers
-cudaError_t launch_gather_rows(const double* X, long long n_local, long long row_lo, int d,
+// X is f64 (elem 8) or f32 (elem 4) rows
+cudaError_t launch_gather_rows(const void* X, int elem, long long n_local, long long row_lo, int d,
                                const long long* ids, int count, double* out, cudaStream_t s);
-cudaError_t launch_kpp_update(const double* X, long long n, int d, const double* c, double* d2,
+cudaError_t launch_kpp_update(const void* X, int elem, long long n, int d, const double* c, double* d2,
                               int first, double* block_sums, int nblk, cudaStream_t s);
 cudaError_t launch_kpp_psums(const double* d2, long long n, double total, double* block_sums,
                              int nblk, cudaStream_t s);
@@ -104,7 +170,7 @@ cudaError_t launch_set_means(const double* src, int k, int d, FinalArgs f, int f
 cudaError_t launch_validate(const double* X, long long n, int d, int k, const int32_t* assign,
                             const double* upper, const double* means, long long* bad,
                             cudaStream_t s);
-cudaError_t launch_check_finite(const double* X, long long n, int d, long long* first_bad,
+cudaError_t launch_check_finite(const void* X, int elem, long long n, int d, long long* first_bad,
                                 cudaStream_t s);
 
 constexpr int KPP_BLOCK = 4096;  // rows per kmeans++ probability block

@@ -74,6 +74,21 @@ __global__ void finalize_kernel(const FinalArgs f) {
   double* m = f.means + (long long)j * d;
   double* pv = f.prev + (long long)j * d;
   const bool occ = cntj > 0.0;
+  if (f.wcss_mode == 2) {
+    // unpruned WCSS against the centroids the pass assigned with (engine.py:331-333),
+    // from the running totals of the new assignment: sum ||x - c||^2 over the
+    // cluster = Q - 2 c.S + count ||c||^2 (tensor-core pass: no per-row exact distance)
+    double cs = 0.0, cc = 0.0;
+    for (int e = lane; e < d; e += 32) {
+      const double o = m[e];
+      cs += o * sums[e];
+      cc += o * o;
+    }
+    cs = warp_sum(cs);
+    cc = warp_sum(cc);
+    if (lane == 0) f.wterm[j] = occ ? sqj - 2.0 * cs + cntj * cc : 0.0;
+    __syncwarp();
+  }
   for (int e = lane; e < d; e += 32) {
     const double old = m[e];
     pv[e] = old;
@@ -86,7 +101,7 @@ __global__ void finalize_kernel(const FinalArgs f) {
     const double n2 = exact_self_rt(m, d);
     f.cn2[j] = n2;
     f.chn[j] = -0.5 * n2;
-    if (f.pruning) {  // sq - ||sums||^2 / count, clamped at 0 (engine.py:385-388)
+    if (f.wcss_mode == 1) {  // sq - ||sums||^2 / count, clamped at 0 (engine.py:385-388)
       double s2 = 0.0;
       for (int e = 0; e < d; ++e) s2 += sums[e] * sums[e];
       const double term = sqj - s2 / cntj;
@@ -105,7 +120,7 @@ __global__ void stats_kernel(const FinalArgs f) {
   double cs = 0.0, ws = 0.0, mx = 0.0;
   for (int j = tid; j < k; j += blockDim.x) {
     cs += f.counts[j];
-    if (f.pruning) ws += f.wterm[j];
+    if (f.wcss_mode) ws += f.wterm[j];
     mx = fmax(mx, f.cn2[j]);
   }
   cs = warp_sum(cs);
@@ -122,7 +137,7 @@ __global__ void stats_kernel(const FinalArgs f) {
     IterStatsDev st;
     st.t = t;
     st.reassignments = (long long)scal[S_REASSIGNED];
-    st.wcss = f.pruning ? W : scal[S_WCSS];
+    st.wcss = f.wcss_mode ? W : scal[S_WCSS];
     st.dist_comps = (long long)scal[S_COMPUTED];
     st.skips = (long long)scal[S_SKIPS];
     st.pruned_stale = (long long)scal[S_PSTALE];

@@ -161,25 +161,46 @@ def torch_stream(device: int) -> int:
     return h or 1
 
 
-def _rows_of(matrix):
-    """numpy -> host rows (validated shape, f64); torch CUDA tensor -> device rows (zero copy)."""
+def _rows_of(matrix, cfg: EngineConfig):
+    """numpy -> host rows (validated shape); torch CUDA tensor -> device rows (zero copy).
+
+    Rows are f64 like the reference's check_matrix (matrix.py:40), except f32 input on a
+    configuration the f32 tensor-core path serves (``_native.f32_supported``): it stays
+    f32 -- the reference's upcast is exact, so nothing changes but the bytes moved."""
     try:
         import torch  # noqa: F401
         is_tensor = type(matrix).__module__.startswith("torch")
     except ImportError:  # pragma: no cover
         is_tensor = False
+
+    def keep_f32(dtype_is_f32, d):
+        return dtype_is_f32 and _native.f32_supported(d, cfg.k, cfg.pruning)
+
     if is_tensor:
+        import torch
         t = matrix
         if t.dim() != 2:
             raise MatrixFormatError(f"expected a 2-D matrix, got ndim={t.dim()}")
         if t.shape[0] < 1 or t.shape[1] < 1:
             raise MatrixFormatError(f"matrix must be at least 1x1, got {t.shape[0]}x{t.shape[1]}")
         if not t.is_cuda:
-            return check_shape(t.numpy()), None
-        import torch
-        t = t.to(torch.float64).contiguous()
+            return _rows_of(t.numpy(), cfg)
+        f32 = keep_f32(t.dtype == torch.float32, int(t.shape[1]))
+        t = t.to(torch.float32 if f32 else torch.float64).contiguous()
         return None, t
-    return check_shape(matrix), None
+    a = np.asarray(matrix)
+    if a.ndim == 2 and keep_f32(a.dtype == np.float32, int(a.shape[1])):
+        return check_shape(a, keep_f32=True), None
+    return check_shape(a), None
+
+
+def _attach_rows(ctx, host, dev) -> None:
+    if dev is not None:
+        (ctx.attach_f32 if dev.element_size() == 4 else ctx.attach)(dev.data_ptr())
+    elif host.dtype == np.float32:
+        ctx.upload_f32(host)
+    else:
+        ctx.upload(host)
 
 
 def kmeans(matrix, cfg: EngineConfig) -> KmeansResult:
@@ -191,8 +212,8 @@ def kmeans(matrix, cfg: EngineConfig) -> KmeansResult:
     """
     if cfg.mode != "im":
         raise ValueError("kmeans() runs in-memory; use kmeans_ondisk() for sem mode")
-    host, dev = _rows_of(matrix)
     cfg.validate()
+    host, dev = _rows_of(matrix, cfg)
     return _run(host, dev, cfg, LocalComm(), device=cfg.device)
 
 
@@ -207,8 +228,8 @@ def kmeans_sharded(local_rows, cfg: EngineConfig, comm, n_global: int | None = N
     """
     if cfg.mode != "im":
         raise ValueError("kmeans() runs in-memory; use kmeans_ondisk() for sem mode")
-    host, dev = _rows_of(local_rows)
     cfg.validate()
+    host, dev = _rows_of(local_rows, cfg)
     return _run(host, dev, cfg, comm, device=device, n_global=n_global, context_cls=context_cls)
 
 
@@ -234,10 +255,7 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         exch = comm.make_exchange(ctx.exchange_len(), device)
         if exch is not None:
             ctx.set_exchange(exch.data_ptr(), exch.numel())
-        if dev is not None:
-            ctx.attach(dev.data_ptr())
-        else:
-            ctx.upload(host)
+        _attach_rows(ctx, host, dev)
         bad = ctx.first_nonfinite_row()
         bad_global = comm.allreduce_min_int(row_lo + bad if bad >= 0 else n)
         if bad_global < n:
@@ -310,7 +328,7 @@ class Lloyd:
                  device: int | None = None):
         cfg.validate()
         self.comm = comm or LocalComm()
-        host, dev = _rows_of(rows)
+        host, dev = _rows_of(rows, cfg)
         r = host if host is not None else dev
         self.n_local, self.d = int(r.shape[0]), int(r.shape[1])
         sizes = self.comm.allgather_int(self.n_local)
@@ -331,10 +349,7 @@ class Lloyd:
         self.exch = self.comm.make_exchange(self.ctx.exchange_len(), device)
         if self.exch is not None:
             self.ctx.set_exchange(self.exch.data_ptr(), self.exch.numel())
-        if dev is not None:
-            self.ctx.attach(dev.data_ptr())
-        else:
-            self.ctx.upload(host)
+        _attach_rows(self.ctx, host, dev)
         self.init_rows = device_init(self.ctx, self.comm, self.exch, cfg.init, cfg.k, cfg.seed,
                                      cfg.initial_centroids, self.n, self.row_lo, self.n_local, self.d)
         if ignore_stop:

@@ -31,9 +31,10 @@ class RowRange(NamedTuple):
         return self.stop - self.start
 
 
-def check_shape(m) -> np.ndarray:
-    """Host half of check_matrix: C-contiguous float64, 2-D, n, d >= 1 (no finite scan)."""
-    m = np.ascontiguousarray(m, dtype=np.float64)
+def check_shape(m, keep_f32: bool = False) -> np.ndarray:
+    """Host half of check_matrix: C-contiguous float64 (float32 kept as is when
+    ``keep_f32``), 2-D, n, d >= 1 (no finite scan)."""
+    m = np.ascontiguousarray(m, dtype=np.float32 if keep_f32 else np.float64)
     if m.ndim != 2:
         raise MatrixFormatError(f"expected a 2-D matrix, got ndim={m.ndim}")
     n, d = m.shape

@@ -95,6 +95,41 @@ def uniform_device(n: int, d: int, seed: int, row_lo: int = 0, rows: int | None 
     return out
 
 
+def mixture_device(spec: MixtureSpec, device: int = 0, chunk_rows: int = 1 << 20):
+    """The same mixture law generated in HBM with torch's seeded CUDA generator (the
+    bytes differ from ``mixture``'s numpy stream; used where only the law matters and
+    host generation would dominate, e.g. config 5's 10 GB at full size)."""
+    import torch
+
+    dev = torch.device("cuda", device)
+    g = torch.Generator(device=dev).manual_seed(spec.seed)
+    dt = getattr(torch, spec.dtype)
+    if spec.centers == "uniform":
+        centers = spec.lo + (spec.hi - spec.lo) * torch.rand((spec.k, spec.d), generator=g, device=dev,
+                                                             dtype=torch.float64)
+    elif spec.centers == "normal":
+        centers = torch.randn((spec.k, spec.d), generator=g, device=dev, dtype=torch.float64)
+    else:
+        raise ValueError(f"unknown center law {spec.centers!r}")
+    if isinstance(spec.sigma, tuple):
+        sigma = spec.sigma[0] + (spec.sigma[1] - spec.sigma[0]) * torch.rand(spec.k, generator=g, device=dev,
+                                                                            dtype=torch.float64)
+    else:
+        sigma = torch.full((spec.k,), float(spec.sigma), device=dev, dtype=torch.float64)
+    if spec.dirichlet is None:
+        w = torch.full((spec.k,), 1.0 / spec.k, device=dev, dtype=torch.float64)
+    else:
+        gam = torch._standard_gamma(torch.full((spec.k,), float(spec.dirichlet), device=dev, dtype=torch.float64))
+        w = gam / gam.sum()
+    x = torch.empty((spec.n, spec.d), dtype=dt, device=dev)
+    for a in range(0, spec.n, chunk_rows):
+        b = min(a + chunk_rows, spec.n)
+        lab = torch.multinomial(w, b - a, replacement=True, generator=g)
+        noise = torch.randn((b - a, spec.d), generator=g, device=dev, dtype=torch.float64)
+        x[a:b] = (centers[lab] + sigma[lab, None] * noise).to(dt)
+    return x
+
+
 # BASELINE.json configs; seed = config index (BASELINE.md section 4).
 CONFIGS = {
     "c1": dict(n=200_000, d=16, k=8, init="forgy", pruning=False, max_iters=20, tolerance=0,
@@ -106,7 +141,8 @@ CONFIGS = {
     "c4": dict(n=856_000_000, d=16, k=100, init="forgy", pruning=True, max_iters=20, tolerance=0,
                data=lambda n: uniform(n, 16, 4)),
     "c5": dict(n=10_000_000, d=256, k=1000, init="forgy", pruning=False, max_iters=10, tolerance=0,
-               data=lambda n: mixture(MixtureSpec(n, 256, 1000, 5, "normal", 0, 0, 0.3, None, "float32"))),
+               data=lambda n: mixture(MixtureSpec(n, 256, 1000, 5, "normal", 0, 0, 0.3, None, "float32")),
+               spec=lambda n: MixtureSpec(n, 256, 1000, 5, "normal", 0, 0, 0.3, None, "float32")),
 }
 # Note: config 4's n rows are a prefix-consistent stream, so any n' < n gives the
 # first n' rows of the full matrix; the mixtures are not prefix-consistent in n

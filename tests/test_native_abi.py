@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert lib.knb_version() == 1
     # every declared symbol has a Python binding signature (or is version/last_error)
-    unbound = [n for n in names if n not in _native.SIGNATURES and n not in ("knb_version", "knb_last_error")]
+    unbound = [n for n in names if n not in _native.SIGNATURES and n not in ("knb_version", "knb_last_error", "knb_f32_supported")]
     assert not unbound, unbound
 
 
@@ -50,3 +50,15 @@ def test_error_path_without_gpu_is_loud():
     from paper_1606_08905_b200 import _native
     with pytest.raises((RuntimeError, ValueError)):
         _native.Context(0, 10, 10, 0, 2, 2, False, 5, 0.0)
+
+
+def test_f32_path_rule():
+    """The f32 tensor-core path (config 5) applies to dense runs with 32 <= d <= 256,
+    d % 4 == 0; everything else is upcast to f64 like the reference's check_matrix."""
+    from paper_1606_08905_b200 import _native
+    assert _native.f32_supported(256, 1000, False)
+    assert _native.f32_supported(32, 8, False)
+    assert not _native.f32_supported(256, 1000, True)
+    assert not _native.f32_supported(16, 8, False)
+    assert not _native.f32_supported(258, 8, False)
+    assert not _native.f32_supported(260, 8, False)
