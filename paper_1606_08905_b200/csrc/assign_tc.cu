@@ -8,9 +8,11 @@
 //   score    s_j = x . c_j - ||c_j||^2 / 2 from one kind::tf32 UMMA per 128 rows x
 //            256 centroids x 8 dims, accumulated in TMEM (argmax s == argmin d)
 //   bound    |s~_j - s_j| <= T(x) = e ||x|| cmax + (f32 rounding) + (reference
-//            rounding slop), e = 2^-8 (TF32 keeps 10 mantissa bits of each
-//            operand: 2^-10 + 2^-10 relative per product, plus the f32 sums; the
-//            factor two of headroom is checked on the GPU by the tests)
+//            rounding slop), e = 1.25 * 2^-9: the tensor core TRUNCATES each f32
+//            operand to 10 mantissa bits (< 2^-10 relative each, measured by
+//            tools/tf32_probe.py), products are exact in f32, and the f32 sums add
+//            < 2^-15 of sum |x_i c_i|; the tests check measured errors stay under
+//            e / 2 on adversarial inputs
 //   certify  s~_1 - s~_2 > 2 T(x): the tensor-core argmax IS the reference's
 //            argmin -- written directly
 //   rerank   otherwise every centroid with s~_j >= s~_1 - 2 T(x) (up to seven, else
@@ -52,10 +54,10 @@ namespace {
 constexpr int TC_M = 128;
 constexpr int TC_N = 256;
 constexpr int TC_KC = 32;
-constexpr int TC_BST = 3;
+constexpr int TC_BST = 6;
 constexpr int TC_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr uint32_t A_CHUNK = TC_M * 128;
-constexpr uint32_t B_CHUNK = TC_N * 128;
+constexpr uint32_t B_CHUNK = (TC_N / 2) * 128;  // this CTA's half of a centroid chunk
 
 constexpr int LIST = 7;  // candidates a queue entry carries (row + 7 ids); more -> all k
 constexpr int TOPK = 8;  // window scores kept per row (and per epilogue half)
@@ -89,7 +91,7 @@ struct Top {
   }
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_assign_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmC,
                      const TcArgs a) {
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();  // CTA pair: rank 0 issues the M = 256 MMAs
+  const bool leader = rank == 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.nkc; ++i) {
       mbar_init(a_full + i, 1);
@@ -118,13 +122,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(t_full + b, 1);
-      mbar_init(t_empty + b, 8);  // one arrival per epilogue warp
+      mbar_init(t_empty + b, 16);  // one arrival per epilogue warp of both CTAs
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tslot, 2 * TC_N);
-    tmem_relinquish();
+    tmem_alloc2(tslot, 2 * TC_N);
+    tmem_relinquish2();
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
@@ -132,40 +136,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const long long ntm = (a.n + TC_M - 1) / TC_M;
+  // pair tiles of 256 rows: this CTA owns rows [256 pt + 128 rank, + 128)
+  const long long ntp = (a.n + 2 * TC_M - 1) / (2 * TC_M);
+  const long long pt0 = blockIdx.x >> 1, ptstep = gridDim.x >> 1;
 
   if (warp == 0) {
-    if (lane == 0) {  // row tiles
+    if (lane == 0) {  // row tiles (both CTAs; completion counted at the leader)
       int it = 0;
-      for (long long mt = blockIdx.x; mt < ntm; mt += gridDim.x, ++it) {
+      for (long long pt = pt0; pt < ntp; pt += ptstep, ++it) {
         for (int kc = 0; kc < a.nkc; ++kc) {
           mbar_wait(a_empty + kc, (it & 1) ^ 1);
-          mbar_arrive_expect_tx(a_full + kc, A_CHUNK);
-          tma_load_2d(A + kc * A_CHUNK, &tmX, a_full + kc, kc * TC_KC, (int)(mt * TC_M));
+          if (leader) mbar_arrive_expect_tx(a_full + kc, 2 * A_CHUNK);
+          tma_load_2d_pair(A + kc * A_CHUNK, &tmX, a_full + kc, kc * TC_KC, (int)(pt * 2 * TC_M + rank * TC_M));
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // centroid chunks
+    if (lane == 0) {  // centroid chunks: this CTA loads centroids [256 nt + 128 rank, + 128)
       int s = 0;
       uint32_t ph = 0;
-      for (long long mt = blockIdx.x; mt < ntm; mt += gridDim.x)
+      for (long long pt = pt0; pt < ntp; pt += ptstep)
         for (int nt = 0; nt < a.nnt; ++nt)
           for (int kc = 0; kc < a.nkc; ++kc) {
             mbar_wait(b_empty + s, ph ^ 1);
-            mbar_arrive_expect_tx(b_full + s, B_CHUNK);
-            tma_load_2d(Bs + s * B_CHUNK, &tmC, b_full + s, kc * TC_KC, nt * TC_N);
+            if (leader) mbar_arrive_expect_tx(b_full + s, 2 * B_CHUNK);
+            tma_load_2d_pair(Bs + s * B_CHUNK, &tmC, b_full + s, kc * TC_KC, nt * TC_N + (int)rank * (TC_N / 2));
             if (++s == TC_BST) { s = 0; ph ^= 1; }
           }
     }
   } else if (warp == 2) {
-    if (lane == 0) {  // MMA issuer
-      const uint32_t idesc = umma_idesc_tf32(TC_M, TC_N);
+    if (lane == 0 && leader) {  // MMA issuer (M = 256 across the pair, N = 256)
+      const uint32_t idesc = umma_idesc_tf32(2 * TC_M, TC_N);
       int s = 0, it = 0;
       uint32_t ph = 0, u = 0;
-      for (long long mt = blockIdx.x; mt < ntm; mt += gridDim.x, ++it) {
+      for (long long pt = pt0; pt < ntp; pt += ptstep, ++it) {
         for (int nt = 0; nt < a.nnt; ++nt, ++u) {
           const uint32_t ab = u & 1;
           mbar_wait(t_empty + ab, ((u >> 1) & 1) ^ 1);
@@ -178,13 +185,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t abase = smem_u32(A + kc * A_CHUNK), bbase = smem_u32(Bs + s * B_CHUNK);
 #pragma unroll
             for (int k4 = 0; k4 < TC_KC / 8; ++k4)
-              umma_tf32(dt, umma_desc_sw128(abase + k4 * 32), umma_desc_sw128(bbase + k4 * 32), idesc,
-                        (kc | k4) != 0);
-            umma_commit(b_empty + s);
-            if (nt == a.nnt - 1) umma_commit(a_empty + kc);
+              umma_tf32_pair(dt, umma_desc_sw128(abase + k4 * 32), umma_desc_sw128(bbase + k4 * 32), idesc,
+                             (kc | k4) != 0);
+            umma_commit_pair(b_empty + s);
+            if (nt == a.nnt - 1) umma_commit_pair(a_empty + kc);
             if (++s == TC_BST) { s = 0; ph ^= 1; }
           }
-          umma_commit(t_full + ab);
+          umma_commit_pair(t_full + ab);
         }
       }
     }
@@ -206,8 +213,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned long long moved = 0, flagged = 0, fulls = 0;
     uint32_t u = 0;
     int par = 0;
-    for (long long mt = blockIdx.x; mt < ntm; mt += gridDim.x, par ^= 1) {
-      const long long row = mt * TC_M + r;
+    for (long long pt = pt0; pt < ntp; pt += ptstep, par ^= 1) {
+      const long long row = pt * 2 * TC_M + rank * TC_M + r;
       const bool valid = row < a.n;
       int old = 0;
       double xn2 = 0.0, T = 0.0;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(t_empty + ab);
+        if (lane == 0) mbar_arrive_leader(t_empty + ab);
       }
       if (a.dbg) continue;
       // ---- merge the two halves of the row (half 1 -> scratch -> half 0)
@@ -401,9 +408,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // the peer's MMAs and TMEM reads are done
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 2 * TC_N);
+    tmem_dealloc2(tmem, 2 * TC_N);
   }
 }
 
@@ -451,18 +459,20 @@ __device__ __forceinline__ double warp_exact_sq(const float* __restrict__ x, con
 // queued row, one warp-wide exact distance per candidate (or per centroid when the
 // candidate list overflowed); the lexicographic (distance, id) minimum is the
 // reference's strict-less ascending scan (distance.py:114-116).
-__global__ void __launch_bounds__(256) tc_rerank_kernel(const float* __restrict__ X, int d, int k,
+__global__ void __launch_bounds__(128) tc_rerank_kernel(const float* __restrict__ X, int d, int k,
                                                         const double* __restrict__ means, int32_t* assign,
                                                         const int32_t* __restrict__ old_assign,
                                                         const int4* __restrict__ queue, const int* qcount,
                                                         long long qcap, unsigned long long* counters,
                                                         float* __restrict__ bound, const Ctrl* ctrl) {
   if (ctrl->stop && !ctrl->ignore_stop) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  const int wstep = gridDim.y * (blockDim.x >> 5);
+  const int w0 = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int cnt = qcount[blockIdx.x];
   const int4* base = queue + 2 * (long long)blockIdx.x * qcap;
   unsigned long long moved = 0;
-  for (int i = warp; i < cnt; i += 8) {
+  for (int i = w0; i < cnt; i += wstep) {
     const int4 e0 = base[2 * i], e1 = base[2 * i + 1];
     const long long row = e0.x;
     const float* x = X + row * d;
@@ -545,12 +555,12 @@ cudaError_t launch_tc_assign(const CUtensorMap* tmX, const CUtensorMap* tmC, con
   const size_t sm = tc_smem_bytes(a.nkc);
   cudaError_t e = cudaFuncSetAttribute(tc_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  tc_assign_kernel<<<grid, TC_THREADS, sm, s>>>(*tmX, *tmC, a);
+  tc_assign_kernel<<<grid, TC_THREADS, sm, s>>>(*tmX, *tmC, a);  // grid even: CTA pairs
   return cudaGetLastError();
 }
 
 cudaError_t launch_tc_rerank(const TcArgs& a, const double* means, int regions, cudaStream_t s) {
-  tc_rerank_kernel<<<regions, 256, 0, s>>>(a.X, a.d, a.k, means, a.assign, a.old_assign, a.queue, a.qcount,
+  tc_rerank_kernel<<<dim3(regions, 16), 128, 0, s>>>(a.X, a.d, a.k, means, a.assign, a.old_assign, a.queue, a.qcount,
                                            a.qcap, a.counters, a.bound, a.ctrl);
   return cudaGetLastError();
 }

@@ -29,7 +29,7 @@ namespace knb {
 namespace {
 
 constexpr int SEG_R = 4096;   // rows per local block
-constexpr int SEG_CH = 2048;  // entries per work item
+constexpr int SEG_CH = 256;   // entries per work item
 
 __device__ __forceinline__ bool seg_stopped(const Ctrl* c) { return c->stop && !c->ignore_stop; }
 
@@ -106,17 +106,45 @@ __global__ void seg_scan_blocks_kernel(SegArgs a) {
 // single CTA: cluster starts and work-item starts (exclusive scans over k)
 __global__ void seg_scan_clusters_kernel(SegArgs a) {
   if (seg_stopped(a.ctrl)) return;
-  if (threadIdx.x == 0) {
-    int s = 0, it = 0;
-    for (int c = 0; c < a.k; ++c) {
-      a.cstart[c] = s;
-      a.istart[c] = it;
-      const int t = a.ctot[c];
-      s += t;
-      it += (t + SEG_CH - 1) / SEG_CH;
+  __shared__ int ws[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  int carry_s = 0, carry_i = 0;
+  for (int base = 0; base < a.k; base += blockDim.x) {
+    const int c = base + tid;
+    const int t = c < a.k ? a.ctot[c] : 0;
+    const int it = (t + SEG_CH - 1) / SEG_CH;
+    int xs = t, xi = it;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ys = __shfl_up_sync(0xffffffffu, xs, o), yi = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) { xs += ys; xi += yi; }
     }
-    a.cstart[a.k] = s;
-    a.istart[a.k] = it;
+    if (lane == 31) { ws[0][w] = xs; ws[1][w] = xi; }
+    __syncthreads();
+    if (w == 0) {
+      int ss = lane < nw ? ws[0][lane] : 0, si = lane < nw ? ws[1][lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ys = __shfl_up_sync(0xffffffffu, ss, o), yi = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) { ss += ys; si += yi; }
+      }
+      ws[0][lane] = ss;
+      ws[1][lane] = si;
+    }
+    __syncthreads();
+    const int bs = (w ? ws[0][w - 1] : 0) + xs - t, bi = (w ? ws[1][w - 1] : 0) + xi - it;
+    if (c < a.k) {
+      a.cstart[c] = carry_s + bs;
+      a.istart[c] = carry_i + bi;
+    }
+    const int ts = ws[0][nw - 1], ti = ws[1][nw - 1];
+    __syncthreads();
+    carry_s += ts;
+    carry_i += ti;
+  }
+  if (tid == 0) {
+    a.cstart[a.k] = carry_s;
+    a.istart[a.k] = carry_i;
   }
 }
 
@@ -161,14 +189,15 @@ __global__ void seg_items_kernel(SegArgs a) {
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     double s = 0.0;
     long long i = e0;
-    for (; i + 4 <= e1; i += 4) {
-      const long long q0 = a.sorted[i], q1 = a.sorted[i + 1], q2 = a.sorted[i + 2], q3 = a.sorted[i + 3];
-      const double v0 = (double)X[(q0 >> 1) * d + e], v1 = (double)X[(q1 >> 1) * d + e];
-      const double v2 = (double)X[(q2 >> 1) * d + e], v3 = (double)X[(q3 >> 1) * d + e];
-      s += (q0 & 1) ? -v0 : v0;
-      s += (q1 & 1) ? -v1 : v1;
-      s += (q2 & 1) ? -v2 : v2;
-      s += (q3 & 1) ? -v3 : v3;
+    for (; i + 8 <= e1; i += 8) {  // eight row loads in flight, summed in entry order
+      long long q[8];
+      double v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) q[t] = a.sorted[i + t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = (double)X[(q[t] >> 1) * d + e];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) s += (q[t] & 1) ? -v[t] : v[t];
     }
     for (; i < e1; ++i) {
       const long long q = a.sorted[i];
@@ -224,7 +253,7 @@ cudaError_t launch_segsum(const SegArgs& a, int elem, cudaStream_t s) {
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   seg_scan_blocks_kernel<<<a.k, 256, 0, s>>>(a);
-  seg_scan_clusters_kernel<<<1, 32, 0, s>>>(a);
+  seg_scan_clusters_kernel<<<1, 1024, 0, s>>>(a);
   {
     long long blocks = (a.n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
