@@ -197,15 +197,18 @@ def run_ours(args):
     tf32_peak = 0.5 * (peaks.get("bf16_tflops") or 2250.0) * 1e12
 
     clocks = Clocks(local_rank)
-    total_iters = args.warmup + args.steps + 2
+    total_iters = args.warmup + 2 * args.steps + 2
     ecfg = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"], max_iters=total_iters,
                            tolerance=cfg["tolerance"], device=local_rank)
     t_init = time.perf_counter()
     run = kb.Lloyd(dev_rows, ecfg, comm=comm, ignore_stop=True, device=local_rank)
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t_init
-    for _ in range(args.warmup):
-        run.step()
+    if world == 1:
+        run.ctx.enqueue(args.warmup)  # iteration 0, then the graph is captured and replayed
+    else:
+        for _ in range(args.warmup):
+            run.step()
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -213,17 +216,26 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     start.record(stream)
+    if world == 1:
+        run.ctx.enqueue(args.steps)  # one CUDA graph replay per iteration
+    else:
+        for i in range(args.steps):
+            run.local()
+            run.exchange()  # NCCL all-reduce of the accumulator vector
+            run.finish()
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = start.elapsed_time(stop)
+    # the local pass alone (the dominant kernel + its merge), same run, next K steps
     for i in range(args.steps):
         ev[i][0].record(stream)
         run.local()
         ev[i][1].record(stream)
         run.exchange()
         run.finish()
-    stop.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    ms = start.elapsed_time(stop)
     local_ms = [a.elapsed_time(b) for a, b in ev]
     if world > 1:
         ms = max(comm.allgather_float(ms))

@@ -130,6 +130,11 @@ int knb_run(knb_ctx* ctx, int32_t batch, int32_t* iterations_done);
 /* EngineConfig.validate_bounds test mode (engine.py:428-445), between local and finish:
  * first row whose assignment != exhaustive argmin and first row whose bound is below its
  * true distance (-1 when none). */
+/* Enqueue up to `count` iterations (fewer at max_iters) without synchronising: iterations
+ * after the first replay one captured CUDA graph (local pass + finish, every decision on
+ * device).  Single-GPU only -- a multi-GPU caller all-reduces between knb_iter_local and
+ * knb_iter_finish instead.  The bench's timed loop. */
+int knb_enqueue(knb_ctx* ctx, int32_t count);
 int knb_validate(knb_ctx* ctx, int64_t* bad_assign_row, int64_t* bad_bound_row);
 
 /* Results: IterationStats rows so far, CentroidSet (centroids.py:15-52), assignments

@@ -76,6 +76,7 @@ SIGNATURES = {
     "knb_iter_finish": [_P],
     "knb_iterate": [_P, ctypes.POINTER(IterStatsC)],
     "knb_run": [_P, _I32, _PI32],
+    "knb_enqueue": [_P, _I32],
     "knb_validate": [_P, _PI64, _PI64],
     "knb_get_stats": [_P, ctypes.POINTER(IterStatsC), _I32, _PI32],
     "knb_get_state": [_P, _PI32, _PI32, _PI64, _PI32],
@@ -273,6 +274,10 @@ class Context:
         v = ctypes.c_int32()
         check(self.L.knb_run(self.h, batch, ctypes.byref(v)))
         return int(v.value)
+
+    def enqueue(self, count: int) -> None:
+        """Queue ``count`` iterations (graph replays after the first); no host sync."""
+        check(self.L.knb_enqueue(self.h, count))
 
     def validate(self) -> tuple[int, int]:
         a, b = ctypes.c_int64(), ctypes.c_int64()

@@ -47,6 +47,11 @@ struct knb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // one steady-state iteration (t >= 1: MTI / delta pass + finish) as a CUDA graph,
+  // replayed by knb_run / knb_enqueue; rebuilt when buffers or options change
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  bool graph_valid = false;
   long long n_global = 0, n_local = 0, row_lo = 0;
   int d = 0, k = 0, pruning = 0, max_iters = 1;
   double tolerance = 0.0;
@@ -291,6 +296,7 @@ int tc_setup(knb_ctx* c) {
 
 int tc_attach(knb_ctx* c, const float* p) {
   c->X32 = p;
+  c->graph_valid = false;
   c->xn_valid = false;
   if (reinterpret_cast<uintptr_t>(p) & 15) return fail(KNB_E_ARG, "f32 rows must be 16-byte aligned");
   if (c->n_local > 0) return encode_f32_map(&c->tmX32, p, c->d, c->n_local, tc_rows_per_tile());
@@ -466,6 +472,58 @@ int install_means(knb_ctx* c, const double* src_dev, int from_partition) {
   return KNB_OK;
 }
 
+// Capture one steady-state iteration into c->graph (the kernels take every decision
+// from device state, so the same graph serves every later iteration of the run).
+int build_graph(knb_ctx* c) {
+  if (c->graph_valid) return KNB_OK;
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  if (!c->cap_stream) KNB_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  if (c->tc) {  // the f32 path computes its row norms once, outside the graph
+    int rc = ensure_xn2(c);
+    if (rc) return rc;
+  }
+  cudaStream_t user = c->stream;
+  const long long t = c->t_host;
+  c->stream = c->cap_stream;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal);
+  int rc = KNB_OK;
+  if (e == cudaSuccess) {
+    rc = launch_local(c);
+    if (!rc) rc = launch_finish(c);
+    e = cudaStreamEndCapture(c->cap_stream, &g);
+  }
+  c->stream = user;
+  c->t_host = t;
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(KNB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(KNB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  c->graph_valid = true;
+  return KNB_OK;
+}
+
+// enqueue one iteration: the captured graph once past the first (full) pass
+int enqueue_iteration(knb_ctx* c) {
+  if (c->t_host >= 1) {
+    int rc = build_graph(c);
+    if (rc) return rc;
+    KNB_CUDA(cudaGraphLaunch(c->graph, c->stream));
+    c->t_host += 1;
+    return KNB_OK;
+  }
+  int rc = launch_local(c);
+  if (rc) return rc;
+  return launch_finish(c);
+}
+
 void to_host_stats(const IterStatsDev& s, knb_iter_stats* o) {
   o->t = s.t;
   o->reassignments = s.reassignments;
@@ -609,6 +667,8 @@ int knb_destroy(knb_ctx* c) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (c->own_exch && c->exch) cudaFree(c->exch);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return KNB_OK;
@@ -694,6 +754,7 @@ int knb_attach_rows(knb_ctx* c, const double* dev) {
   if (c->tc) return fail(KNB_E_STATE, "context holds f32 rows");
   KNB_CUDA(cudaSetDevice(c->device));
   c->X = dev;
+  c->graph_valid = false;
   return build_tmap(c);
 }
 
@@ -725,6 +786,7 @@ int knb_set_exchange(knb_ctx* c, double* dev, int64_t len) {
     c->bytes -= (long long)(c->L * sizeof(double));
   }
   c->exch = dev;
+  c->graph_valid = false;
   c->own_exch = false;
   return KNB_OK;
 }
@@ -914,10 +976,8 @@ int knb_run(knb_ctx* c, int32_t batch, int32_t* done) {
   if (batch < 1) batch = 1;
   Ctrl h;
   for (;;) {
-    for (int b = 0; b < batch && c->t_host < c->max_iters; ++b) {
-      if ((rc = launch_local(c))) return rc;
-      if ((rc = launch_finish(c))) return rc;
-    }
+    for (int b = 0; b < batch && c->t_host < c->max_iters; ++b)
+      if ((rc = enqueue_iteration(c))) return rc;
     KNB_CUDA(cudaMemcpyAsync(&h, c->ctrl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     KNB_CUDA(cudaStreamSynchronize(c->stream));
     if (h.count_error)
@@ -926,6 +986,14 @@ int knb_run(knb_ctx* c, int32_t batch, int32_t* done) {
     if ((h.stop && !h.ignore_stop) || c->t_host >= c->max_iters) break;
   }
   if (done) *done = (int32_t)h.t;
+  return KNB_OK;
+}
+
+int knb_enqueue(knb_ctx* c, int32_t count) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  for (int b = 0; b < count && c->t_host < c->max_iters; ++b)
+    if ((rc = enqueue_iteration(c))) return rc;
   return KNB_OK;
 }
 
@@ -1036,6 +1104,7 @@ int knb_set_option(knb_ctx* c, int32_t option, int64_t value) {
     if ((value == KNB_MTI_DENSE || value == KNB_MTI_BLOCK) && !c->mti_mma_ok)
       return fail(KNB_E_ARG, "dense MTI scan needs d <= 64 and centroids that fit shared memory");
     c->mti_scan = (int)value;
+    c->graph_valid = false;
     return KNB_OK;
   }
   return fail(KNB_E_ARG, "unknown option " + std::to_string(option));

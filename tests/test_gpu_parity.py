@@ -69,9 +69,10 @@ def test_gpu_tensor_core_mti_matches_reference_golden(name, mode):
             assert s.pruned_stale == 0 and s.pruned_tight == 0
 
 
-@pytest.mark.parametrize("name", ["c1_full", "c3_mini", "kpp_pruned", "d33_pruned", "d65_dense"])
+@pytest.mark.parametrize("name", ["c1_full", "c3_mini", "kpp_pruned", "d33_pruned", "d65_dense", "c5_mini", "unif_pruned"])
 def test_gpu_batched_run_equals_stepwise(name):
-    """The batched single-GPU loop (device stop flag) == the per-iteration loop."""
+    """The batched single-GPU loop (CUDA-graph replays, device stop flag) == the
+    per-iteration loop."""
     m = case_data(name)
     a = kb.kmeans(m, _cfg(name, batch=7))
     b = kb.kmeans(m, _cfg(name, collect_assignments=True))
