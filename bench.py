@@ -199,7 +199,7 @@ def run_ours(args):
     clocks = Clocks(local_rank)
     total_iters = args.warmup + 2 * args.steps + 2
     ecfg = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"], max_iters=total_iters,
-                           tolerance=cfg["tolerance"], device=local_rank)
+                           tolerance=cfg["tolerance"], device=local_rank, mti_scan=args.mti_scan)
     t_init = time.perf_counter()
     run = kb.Lloyd(dev_rows, ecfg, comm=comm, ignore_stop=True, device=local_rank)
     torch.cuda.synchronize()
@@ -372,6 +372,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-reps", type=int, default=2)
+    ap.add_argument("--mti-scan", default="auto", help="EngineConfig.mti_scan for the timed run (experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 warm-up steps
