@@ -113,6 +113,13 @@ int knb_init_partition_finish(knb_ctx* ctx);
 int knb_kpp_update(knb_ctx* ctx, int32_t first, double* local_total);
 int knb_kpp_psum(knb_ctx* ctx, double total, double* local_psum);
 int knb_kpp_search(knb_ctx* ctx, double total, double threshold, int64_t* local_idx);
+/* Single-GPU kmeans++ in one call: first_pick = rng.integers(n) and u[0..k-2] = the next
+ * k - 1 rng.random() draws of the host stream (centroids.py:174-189 consumes exactly these
+ * while the D^2 total stays > 0); the D^2 updates, totals, cumulative sums and searches run
+ * on the device without host round trips, then the k rows are installed.  *degenerate = 1
+ * (nothing installed) when a total is 0 -- the caller replays the reference's draw order
+ * with the step-wise calls below. */
+int knb_kpp_run(knb_ctx* ctx, int64_t first_pick, const double* u, int32_t k, int64_t* picks, int32_t* degenerate);
 int knb_kpp_release(knb_ctx* ctx);
 
 /* One Lloyd iteration, split around the cross-GPU exchange:

@@ -72,6 +72,7 @@ SIGNATURES = {
     "knb_kpp_psum": [_P, _D, _PD],
     "knb_kpp_search": [_P, _D, _D, _PI64],
     "knb_kpp_release": [_P],
+    "knb_kpp_run": [_P, _I64, _P, _I32, _P, _PI32],
     "knb_iter_local": [_P],
     "knb_iter_finish": [_P],
     "knb_iterate": [_P, ctypes.POINTER(IterStatsC)],
@@ -135,6 +136,21 @@ def check(rc: int) -> None:
 
 def ptr(a: np.ndarray) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.ctypes.data)
+
+
+def _host_buffer(count: int, dtype) -> np.ndarray:
+    """Result array for a device->host copy: page-locked (torch's pinned allocator) when
+    large, so the D2H runs at link speed instead of through a bounce buffer."""
+    if count * np.dtype(dtype).itemsize >= (4 << 20):
+        try:
+            import torch
+            if torch.cuda.is_available():
+                t = torch.empty(count, dtype={np.int32: torch.int32, np.float64: torch.float64}[dtype],
+                                pin_memory=True)
+                return t.numpy()  # shares the pinned buffer and keeps it alive
+        except Exception:  # pragma: no cover - pinned memory is an optimisation only
+            pass
+    return np.empty(count, dtype=dtype)
 
 
 class Context:
@@ -255,6 +271,15 @@ class Context:
         check(self.L.knb_kpp_search(self.h, float(total), float(threshold), ctypes.byref(v)))
         return int(v.value)
 
+    def kpp_run(self, first_pick: int, u: np.ndarray) -> tuple[list[int], bool]:
+        """Single-GPU kmeans++ on the device; returns (picks, degenerate)."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        picks = np.empty(self.k, dtype=np.int64)
+        deg = ctypes.c_int32()
+        check(self.L.knb_kpp_run(self.h, int(first_pick), ptr(u) if u.size else None, self.k, ptr(picks),
+                                 ctypes.byref(deg)))
+        return [int(p) for p in picks], bool(deg.value)
+
     def kpp_release(self) -> None:
         check(self.L.knb_kpp_release(self.h))
 
@@ -309,7 +334,7 @@ class Context:
     def assignments(self, lo: int = 0, count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
         count = self.n_local - lo if count is None else count
         if out is None:
-            out = np.empty(count, dtype=np.int32)
+            out = _host_buffer(count, np.int32)
         check(self.L.knb_get_assignments(self.h, ptr(out), lo, count))
         return out
 

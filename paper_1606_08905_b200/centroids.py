@@ -107,6 +107,14 @@ def device_init(ctx, comm, exch, method: str, k: int, seed: int, initial, n: int
         return None
 
     # kmeans++
+    if comm.world == 1 and hasattr(ctx, "kpp_run"):
+        # one device call: the draws the reference consumes while every D^2 total is > 0
+        first = int(rng.integers(n))
+        picks, degenerate = ctx.kpp_run(first, rng.random(k - 1))
+        if not degenerate:
+            ctx.kpp_release()
+            return picks
+        rng = np.random.default_rng(seed)  # replay the reference's draw order step by step
     picks = [int(rng.integers(n))]
     gather([picks[0]])
     total = comm.allreduce_sum(ctx.kpp_update(first=True))

@@ -415,46 +415,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// Exact distance of one row to one centroid by a whole warp, bit-identical to
-// exact_sq_rt (the OpenBLAS ddot tree of oracle/exact_tree.c): lane 8a + l owns
-// accumulator z[a][l] of the 32-wide blocks, lanes l < 4 then own acc[a][l] of the
-// 16-wide blocks, and the final adds run in the tree's order through shuffles.
-// The result is valid in every lane.
-__device__ __forceinline__ double warp_exact_sq(const float* __restrict__ x, const double* __restrict__ c, int d,
-                                                int lane) {
-  const int n1 = d & ~15, n32 = n1 & ~31;
-  double dot = 0.0;
-  if (n1) {
-    double z = 0.0;
-    for (int i = 0; i < n32; i += 32) {
-      const double v = __dsub_rn((double)x[i + lane], c[i + lane]);
-      z = __fma_rn(v, v, z);
-    }
-    const int a = lane >> 3, l = lane & 7;
-    // acc[a][l] = z[a][l] + z[a][l + 4]   (lanes with l < 4)
-    double acc = __dadd_rn(z, __shfl_down_sync(0xffffffffu, z, 4));
-    for (int i = n32; i < n1; i += 16) {
-      if (l < 4) {
-        const double v = __dsub_rn((double)x[i + 4 * a + l], c[i + 4 * a + l]);
-        acc = __fma_rn(v, v, acc);
-      }
-    }
-    // s[l] = ((acc[0][l] + acc[1][l]) + acc[2][l]) + acc[3][l]   (on lane l < 4)
-    const double a1 = __shfl_down_sync(0xffffffffu, acc, 8);
-    const double a2 = __shfl_down_sync(0xffffffffu, acc, 16);
-    const double a3 = __shfl_down_sync(0xffffffffu, acc, 24);
-    const double sl = __dadd_rn(__dadd_rn(__dadd_rn(acc, a1), a2), a3);
-    const double s0 = __shfl_sync(0xffffffffu, sl, 0), s1 = __shfl_sync(0xffffffffu, sl, 1);
-    const double s2 = __shfl_sync(0xffffffffu, sl, 2), s3 = __shfl_sync(0xffffffffu, sl, 3);
-    dot = __dadd_rn(__dadd_rn(s0, s2), __dadd_rn(s1, s3));
-  }
-  for (int i = n1; i < d; ++i) {
-    const double v = __dsub_rn((double)x[i], c[i]);
-    dot = __fma_rn(v, v, dot);
-  }
-  return dot;
-}
-
 // Exact f64 re-scoring of the rows the certificate could not settle: one warp per
 // queued row, one warp-wide exact distance per candidate (or per centroid when the
 // candidate list overflowed); the lexicographic (distance, id) minimum is the

@@ -927,6 +927,72 @@ int knb_kpp_search(knb_ctx* c, double total, double threshold, int64_t* local_id
   return KNB_OK;
 }
 
+// The whole kmeans++ loop on one GPU (centroids.py:174-189): the host supplies the
+// first pick and the k - 1 uniform draws of its RNG stream; every D^2 update, total,
+// probability block sum and search runs on the device back to back, with one
+// synchronisation at the end.  A step whose D^2 total is 0 (the reference then
+// draws an integer instead) is reported as degenerate and nothing is installed.
+int knb_kpp_run(knb_ctx* c, int64_t first_pick, const double* u_host, int32_t k, int64_t* picks_out,
+                int32_t* degenerate) {
+  int rc = need_ready(c, false);
+  if (rc) return rc;
+  if (k != c->k || !u_host || !picks_out) return fail(KNB_E_ARG, "kpp_run: k must be the context's k");
+  if (c->n_local != c->n_global) return fail(KNB_E_STATE, "kpp_run is single-GPU; sharded runs use kpp_update/psum/search");
+  if (first_pick < 0 || first_pick >= c->n_local) return fail(KNB_E_ARG, "first pick outside [0, n)");
+  if ((rc = kpp_buffers(c))) return rc;
+  long long* picks = nullptr;
+  double* u = nullptr;
+  int* degen = nullptr;
+  double* scal = nullptr;
+  if ((rc = dev_alloc(c, &picks, (size_t)k))) return rc;
+  auto cleanup = [&]() {
+    cudaFree(picks);
+    if (u) cudaFree(u);
+    if (degen) cudaFree(degen);
+    if (scal) cudaFree(scal);
+    c->bytes -= (long long)(k * 8 + (k > 1 ? (k - 1) * 8 : 8) + 4 + 16);
+  };
+  if ((rc = dev_alloc(c, &u, (size_t)(k > 1 ? k - 1 : 1))) || (rc = dev_alloc(c, &degen, 1)) ||
+      (rc = dev_alloc(c, &scal, 2))) {
+    cleanup();
+    return rc;
+  }
+  long long p0 = first_pick;
+  cudaError_t e = cudaMemcpyAsync(picks, &p0, sizeof(p0), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess && k > 1)
+    e = cudaMemcpyAsync(u, u_host, sizeof(double) * (k - 1), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(degen, 0, sizeof(int), c->stream);
+  const void* X = rows_of(c);
+  const int d = c->d;
+  if (e == cudaSuccess) e = launch_gather_row_dev(X, c->elem, d, picks, c->stage, c->stream);
+  for (int i = 1; i < k && e == cudaSuccess; ++i) {
+    // D^2 against centroid i - 1, its fixed-order total, p-block sums, their end, search
+    e = launch_kpp_update(X, c->elem, c->n_local, d, c->stage + (size_t)(i - 1) * d, c->d2, i == 1, c->kpp_bs,
+                          c->kpp_nblk, c->stream);
+    if (e == cudaSuccess) e = launch_sum_blocks(c->kpp_bs, c->kpp_nblk, scal, c->stream);
+    if (e == cudaSuccess) e = launch_kpp_psums_dev(c->d2, c->n_local, scal, c->kpp_bs, c->kpp_nblk, c->stream);
+    if (e == cudaSuccess) e = launch_sum_blocks(c->kpp_bs, c->kpp_nblk, scal + 1, c->stream);
+    if (e == cudaSuccess)
+      e = launch_kpp_search_dev(c->d2, c->n_local, scal, c->kpp_bs, c->kpp_nblk, scal + 1, u + (i - 1), picks + i,
+                                degen, c->stream);
+    if (e == cudaSuccess) e = launch_gather_row_dev(X, c->elem, d, picks + i, c->stage + (size_t)i * d, c->stream);
+  }
+  std::vector<long long> hp((size_t)k);
+  int hd = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hp.data(), picks, sizeof(long long) * k, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hd, degen, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cleanup();
+  if (e != cudaSuccess) return fail(KNB_E_CUDA, std::string("kpp_run: ") + cudaGetErrorString(e));
+  for (int i = 0; i < k; ++i) picks_out[i] = hp[(size_t)i];
+  if (degenerate) *degenerate = hd;
+  if (hd) return KNB_OK;
+  rc = install_means(c, c->stage, 0);
+  if (rc) return rc;
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  return KNB_OK;
+}
+
 int knb_kpp_release(knb_ctx* c) {
   if (!c) return fail(KNB_E_ARG, "null context");
   cudaSetDevice(c->device);

@@ -45,10 +45,57 @@ __global__ void kpp_update_kernel(const T* __restrict__ X, long long n, int d,
   const long long b = blockIdx.x;
   const long long lo = b * KPP_BLOCK;
   double s = 0.0;
+  // thread-strided rows: one sequential exact tree per row (this order also fixes the
+  // block sum the probability walk uses)
   for (int i = threadIdx.x; i < KPP_BLOCK; i += blockDim.x) {
     const long long r = lo + i;
     if (r >= n) break;
     const double dist = sqrt(exact_sq_rt(X + r * d, c, d));
+    const double cand = dist * dist;
+    double v = first ? cand : fmin(d2[r], cand);
+    d2[r] = v;
+    s += v;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    block_sums[b] = t;
+  }
+}
+
+// Same contract and summation order as kpp_update_kernel for f64 rows with d <= DP:
+// the row is loaded into registers with 16-byte loads and the centroid is read from
+// shared memory, so the pass runs at memory speed.
+template <int DP>
+__global__ void kpp_update_reg_kernel(const double* __restrict__ X, long long n, int d, const double* __restrict__ c,
+                                      double* __restrict__ d2, int first, double* __restrict__ block_sums) {
+  __shared__ double sh[32];
+  __shared__ double cs[DP];
+  for (int e = threadIdx.x; e < DP; e += blockDim.x) cs[e] = e < d ? c[e] : 0.0;
+  __syncthreads();
+  const long long b = blockIdx.x;
+  const long long lo = b * KPP_BLOCK;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < KPP_BLOCK; i += blockDim.x) {
+    const long long r = lo + i;
+    if (r >= n) break;
+    double x[DP];
+    const double2* xr = reinterpret_cast<const double2*>(X + r * d);
+#pragma unroll
+    for (int q = 0; q < DP / 2; ++q) {
+      if (2 * q < d) {
+        const double2 v = xr[q];
+        x[2 * q] = v.x;
+        x[2 * q + 1] = v.y;
+      } else {
+        x[2 * q] = 0.0;
+        x[2 * q + 1] = 0.0;
+      }
+    }
+    const double dist = sqrt(exact_sq<DP>(x, cs, d));
     const double cand = dist * dist;
     double v = first ? cand : fmin(d2[r], cand);
     d2[r] = v;
@@ -85,18 +132,72 @@ __global__ void kpp_psums_kernel(const double* __restrict__ d2, long long n, dou
   }
 }
 
-__global__ void sum_blocks_kernel(const double* __restrict__ bs, int nblk, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
+// block sums of p = d2 / total with total read from device memory (device loop)
+__global__ void kpp_psums_dev_kernel(const double* __restrict__ d2, long long n, const double* total_p,
+                                     double* __restrict__ block_sums) {
+  __shared__ double sh[32];
+  const double total = *total_p;
+  const long long lo = blockIdx.x * (long long)KPP_BLOCK;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < KPP_BLOCK; i += blockDim.x) {
+    const long long r = lo + i;
+    if (r >= n) break;
+    s += d2[r] / total;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < nblk; ++i) t += bs[i];
-    *out = t;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    block_sums[blockIdx.x] = t;
   }
 }
 
-// single CTA: walk block sums, then scan inside the crossing block
+// copy row idx[0] of the shard into dst (device-side index)
+template <typename T>
+__global__ void gather_row_dev_kernel(const T* __restrict__ X, int d, const long long* idx, double* __restrict__ dst) {
+  const long long r = *idx;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) dst[e] = (double)X[r * d + e];
+}
+
+// one warp: lane l adds blocks l, l + 32, ... in order, then a fixed butterfly
+__global__ void sum_blocks_kernel(const double* __restrict__ bs, int nblk, double* out) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  double t = 0.0;
+  for (int i = lane; i < nblk; i += 32) t += bs[i];
+  t = warp_sum(t);
+  if (lane == 0) *out = t;
+}
+
+// single CTA: walk block sums, then scan inside the crossing block.  Device-loop
+// form: total, the cumulative end and the uniform draw come from device memory
+// (thr = u * cdf_end, the host's arithmetic); total == 0 flags a degenerate step.
+__device__ void kpp_search_body(const double* __restrict__ d2, long long n, double total,
+                                const double* __restrict__ bs, int nblk, double thr, long long* out);
+
+__global__ void kpp_search_dev_kernel(const double* __restrict__ d2, long long n, const double* total_p,
+                                      const double* __restrict__ bs, int nblk, const double* cdf_p,
+                                      const double* u, long long* out, int* degenerate) {
+  const double total = *total_p;
+  if (!(total > 0.0)) {
+    if (threadIdx.x == 0) {
+      *degenerate = 1;
+      *out = 0;
+    }
+    return;
+  }
+  kpp_search_body(d2, n, total, bs, nblk, *u * *cdf_p, out);
+}
+
 __global__ void kpp_search_kernel(const double* __restrict__ d2, long long n, double total,
-                                  const double* __restrict__ bs, int nblk, double thr,
-                                  long long* out) {
+                                  const double* __restrict__ bs, int nblk, double thr, long long* out) {
+  kpp_search_body(d2, n, total, bs, nblk, thr, out);
+}
+
+__device__ void kpp_search_body(const double* __restrict__ d2, long long n, double total,
+                                const double* __restrict__ bs, int nblk, double thr, long long* out) {
   __shared__ double run_sh;
   __shared__ int blk_sh;
   __shared__ double part[1024];
@@ -189,10 +290,18 @@ cudaError_t launch_gather_rows(const void* X, int elem, long long n_local, long 
 
 cudaError_t launch_kpp_update(const void* X, int elem, long long n, int d, const double* c, double* d2, int first,
                               double* block_sums, int nblk, cudaStream_t s) {
-  if (elem == 4)
+  const bool vec = elem == 8 && (d % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  const double* Xd = static_cast<const double*>(X);
+  if (vec && d <= 8)
+    kpp_update_reg_kernel<8><<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
+  else if (vec && d <= 16)
+    kpp_update_reg_kernel<16><<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
+  else if (vec && d <= 32)
+    kpp_update_reg_kernel<32><<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
+  else if (elem == 4)
     kpp_update_kernel<<<nblk, 256, 0, s>>>(static_cast<const float*>(X), n, d, c, d2, first, block_sums);
   else
-    kpp_update_kernel<<<nblk, 256, 0, s>>>(static_cast<const double*>(X), n, d, c, d2, first, block_sums);
+    kpp_update_kernel<<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
   return cudaGetLastError();
 }
 
@@ -210,6 +319,25 @@ cudaError_t launch_sum_blocks(const double* block_sums, int nblk, double* out, c
 cudaError_t launch_kpp_search(const double* d2, long long n, double total, const double* block_sums, int nblk,
                               double threshold, long long* out, cudaStream_t s) {
   kpp_search_kernel<<<1, 256, 0, s>>>(d2, n, total, block_sums, nblk, threshold, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kpp_psums_dev(const double* d2, long long n, const double* total, double* block_sums, int nblk,
+                                 cudaStream_t s) {
+  kpp_psums_dev_kernel<<<nblk, 256, 0, s>>>(d2, n, total, block_sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kpp_search_dev(const double* d2, long long n, const double* total, const double* block_sums,
+                                  int nblk, const double* cdf_end, const double* u, long long* out, int* degenerate,
+                                  cudaStream_t s) {
+  kpp_search_dev_kernel<<<1, 256, 0, s>>>(d2, n, total, block_sums, nblk, cdf_end, u, out, degenerate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_row_dev(const void* X, int elem, int d, const long long* idx, double* dst, cudaStream_t s) {
+  if (elem == 4) gather_row_dev_kernel<<<1, 256, 0, s>>>(static_cast<const float*>(X), d, idx, dst);
+  else gather_row_dev_kernel<<<1, 256, 0, s>>>(static_cast<const double*>(X), d, idx, dst);
   return cudaGetLastError();
 }
 

@@ -165,6 +165,13 @@ cudaError_t launch_kpp_psums(const double* d2, long long n, double total, double
 cudaError_t launch_kpp_search(const double* d2, long long n, double total, const double* block_sums,
                               int nblk, double threshold, long long* out, cudaStream_t s);
 cudaError_t launch_sum_blocks(const double* block_sums, int nblk, double* out, cudaStream_t s);
+// kmeans++ with every scalar on the device (single-GPU loop, no host round trips)
+cudaError_t launch_kpp_psums_dev(const double* d2, long long n, const double* total, double* block_sums, int nblk,
+                                 cudaStream_t s);
+cudaError_t launch_kpp_search_dev(const double* d2, long long n, const double* total, const double* block_sums,
+                                  int nblk, const double* cdf_end, const double* u, long long* out, int* degenerate,
+                                  cudaStream_t s);
+cudaError_t launch_gather_row_dev(const void* X, int elem, int d, const long long* idx, double* dst, cudaStream_t s);
 cudaError_t launch_set_means(const double* src, int k, int d, FinalArgs f, int from_partition,
                              long long n, cudaStream_t s);
 cudaError_t launch_validate(const double* X, long long n, int d, int k, const int32_t* assign,

@@ -230,3 +230,25 @@ def test_config4_shape_sample():
     r = kb.kmeans(m, kb.EngineConfig(k=100, init="forgy", seed=4, pruning=True, max_iters=3))
     assert r.n_iterations == 3
     _stepwise_sample_check(m, r, sample=5000)
+
+
+@pytest.mark.parametrize("n,d,k,seed", [(5000, 5, 20, 1), (20000, 32, 32, 2), (3000, 100, 12, 3), (4000, 3, 50, 4)])
+def test_gpu_kmeanspp_device_loop_matches_oracle(n, d, k, seed):
+    """The single-GPU kmeans++ loop (knb_kpp_run: every D^2 update, total and search on
+    the device) picks exactly the reference's rows (oracle pinned to the reference)."""
+    m = kb.synth.mixture(kb.synth.MixtureSpec(n, d, max(2, k // 2), 40 + seed, "uniform", -4, 4, 1.0))
+    r = kb.kmeans(m, kb.EngineConfig(k=k, init="kmeanspp", seed=seed, pruning=True, max_iters=2))
+    o = O.lloyd(m, k, init="kmeanspp", seed=seed, pruning=True, max_iters=2)
+    np.testing.assert_array_equal(m[np.asarray(r.init_rows)], o.init_means)
+
+
+def test_gpu_kmeanspp_degenerate_total_replays_reference_draws():
+    """Only two distinct points and k = 3: after both are picked every D^2 is 0 and the
+    reference draws rng.integers(n) instead of a weighted choice (centroids.py:182-186);
+    the device loop reports it and the host replays the reference's draw order."""
+    m = np.array([[0.0, 0.0]] * 3 + [[1.0, 1.0]] * 2)
+    for seed in range(6):
+        r = kb.kmeans(m, kb.EngineConfig(k=3, init="kmeanspp", seed=seed, pruning=False, max_iters=3))
+        o = O.lloyd(m, 3, init="kmeanspp", seed=seed, pruning=False, max_iters=3)
+        np.testing.assert_array_equal(m[np.asarray(r.init_rows)], o.init_means)
+        assert np.array_equal(r.centroids.means, o.means)
