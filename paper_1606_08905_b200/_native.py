@@ -138,21 +138,6 @@ def ptr(a: np.ndarray) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.ctypes.data)
 
 
-def _host_buffer(count: int, dtype) -> np.ndarray:
-    """Result array for a device->host copy: page-locked (torch's pinned allocator) when
-    large, so the D2H runs at link speed instead of through a bounce buffer."""
-    if count * np.dtype(dtype).itemsize >= (4 << 20):
-        try:
-            import torch
-            if torch.cuda.is_available():
-                t = torch.empty(count, dtype={np.int32: torch.int32, np.float64: torch.float64}[dtype],
-                                pin_memory=True)
-                return t.numpy()  # shares the pinned buffer and keeps it alive
-        except Exception:  # pragma: no cover - pinned memory is an optimisation only
-            pass
-    return np.empty(count, dtype=dtype)
-
-
 class Context:
     """One GPU shard: owns a knb_ctx and frees it on close()."""
 
@@ -334,7 +319,7 @@ class Context:
     def assignments(self, lo: int = 0, count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
         count = self.n_local - lo if count is None else count
         if out is None:
-            out = _host_buffer(count, np.int32)
+            out = np.empty(count, dtype=np.int32)
         check(self.L.knb_get_assignments(self.h, ptr(out), lo, count))
         return out
 

@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(KNB_NT, 1)
       if (lmask) {
         const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
         int nid = sc.id;
-        double sq = 0.0;
-        const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, &sq);
+        const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr);
+        const double sq = (live && nid != aa) ? row_self_sq<DP>(tb, my_r, d) : 0.0;
         if (live) {
           a.upper[row] = nd;
           a.tight[row] = 1;

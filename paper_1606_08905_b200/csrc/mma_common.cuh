@@ -209,6 +209,20 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
   return nd;
 }
 
+// vecdot(x, x) of tile row r by the exact recipe (row_sqnorms, distance.py:66-72)
+template <int DP>
+__device__ __forceinline__ double row_self_sq(const unsigned char* tb, int r, int d) {
+  using TL = TileLayout<DP>;
+  double x[DP];
+#pragma unroll
+  for (int q2 = 0; q2 < DP / 2; ++q2) {
+    const double2 v = *reinterpret_cast<const double2*>(tb + TL::chunk_off(r, q2, BR));
+    x[2 * q2] = v.x;
+    x[2 * q2 + 1] = v.y;
+  }
+  return exact_sq<DP>(x, Zero{}, d);
+}
+
 // Deterministic warp-local accumulation in row order, lanes = dims.  For every row r
 // set in `rowmask` (ascending; the row's values live in lane owner_lane(r)):
 //   acc[to][e] += x[r][e], cnt[to] += 1, sqa[to] += sq, and when from >= 0 the same

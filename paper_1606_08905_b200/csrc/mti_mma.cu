@@ -134,10 +134,11 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
     const int r = t4 * 8 + g;
     const bool valid = r < cnum;
     int id = sc.id;
-    double sq = 0.0;
-    const double nd = exact_winner<DP>(tb, r, crow, k, d, sc.flag, id, &sq);
+    const double nd = exact_winner<DP>(tb, r, crow, k, d, sc.flag, id, nullptr);
     const int orig = valid ? qorig[r] : 0;
     const bool moved = valid && id != orig;
+    // ||x||^2 only for the (few) moved rows whose signed deltas carry it
+    const double sq = moved ? row_self_sq<DP>(tb, r, d) : 0.0;
     if (valid) {
       const long long grow = qrow[r];
       a.upper[grow] = nd;
