@@ -39,6 +39,19 @@ __device__ __forceinline__ void score_update(double& best, int& bid, bool& flag,
   bid = better ? j : bid;
 }
 
+// merge a partial state whose ids all come after the running one's (ties keep the
+// running, earlier id)
+__device__ __forceinline__ void merge_later(double& best, int& bid, bool& flag, double ob, int oi, bool of,
+                                            int tolhi) {
+  const double diff = __dsub_rn(ob, best);
+  const int h = __double2hiint(diff);
+  const bool near = (h & 0x7fffffff) <= tolhi;
+  const bool other = h > 0;
+  flag = near | (other ? of : flag);
+  best = other ? ob : best;
+  bid = other ? oi : bid;
+}
+
 // merge the disjoint partial (best, id, flag) held by lane ^ lanemask
 __device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int tolhi, int lanemask) {
   const double ob = __shfl_xor_sync(0xffffffffu, best, lanemask);
@@ -146,14 +159,22 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
       }
     }
   };
+  // The step's four scores per row group are first reduced among themselves (two
+  // independent pairs, then a merge), and only the result is merged into the
+  // running state: the loop-carried chain is one merge per step instead of four
+  // updates.  Same result: the argmax (lowest id on ties) and "some other score
+  // within tol of it" do not depend on the order of the merges.
   auto epilogue = [&](int q, const double (&c0)[4][2], const double (&c1)[4][2]) {
     const int j0 = q * 8 + 2 * t4;
 #pragma unroll
     for (int pg = 0; pg < 4; ++pg) {
-      score_update(best[pg], bid[pg], flag[pg], c0[pg][0], j0, tolhi[pg]);
-      score_update(best[pg], bid[pg], flag[pg], c0[pg][1], j0 + 1, tolhi[pg]);
-      score_update(best[pg], bid[pg], flag[pg], c1[pg][0], j0 + 8, tolhi[pg]);
-      score_update(best[pg], bid[pg], flag[pg], c1[pg][1], j0 + 9, tolhi[pg]);
+      double pb = c0[pg][0], qb = c1[pg][0];
+      int pi = j0, qi = j0 + 8;
+      bool pf = false, qf = false;
+      score_update(pb, pi, pf, c0[pg][1], j0 + 1, tolhi[pg]);
+      score_update(qb, qi, qf, c1[pg][1], j0 + 9, tolhi[pg]);
+      merge_later(pb, pi, pf, qb, qi, qf, tolhi[pg]);
+      merge_later(best[pg], bid[pg], flag[pg], pb, pi, pf, tolhi[pg]);
     }
   };
   double ca0[4][2], ca1[4][2], cb0[4][2], cb1[4][2];
