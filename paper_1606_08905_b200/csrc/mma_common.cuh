@@ -15,6 +15,12 @@ namespace knb {
 
 constexpr int BR = 32;  // rows per warp block
 
+// Row stride (doubles) of the exact-recipe centroid copy in shared memory: odd, so the
+// lanes of a warp reading DIFFERENT centroids' element e hit different bank pairs
+// (a DP stride put every lane's element e in the same bank).
+template <int DP>
+__host__ __device__ constexpr int crow_stride() { return DP + 1; }
+
 // not volatile: the mma has no side effects, so ptxas may interleave it with the epilogue
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 #if KNB_EXPERIMENT == 2  // experiment: no tensor work
@@ -218,13 +224,13 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
     double bd = CUDART_INF;
     int bi = 0;
     for (int j = 0; j < k; ++j) {
-      const double dj = sqrt(exact_sq<DP>(x, crow + j * DP, d));
+      const double dj = sqrt(exact_sq<DP>(x, crow + j * crow_stride<DP>(), d));
       if (dj < bd) { bd = dj; bi = j; }
     }
     id = bi;
     nd = bd;
   } else {
-    nd = sqrt(exact_sq<DP>(x, crow + id * DP, d));
+    nd = sqrt(exact_sq<DP>(x, crow + id * crow_stride<DP>(), d));
   }
   if (sq_out) *sq_out = exact_sq<DP>(x, Zero{}, d);
   return nd;

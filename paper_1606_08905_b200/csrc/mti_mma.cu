@@ -39,7 +39,7 @@ struct MtiMmaSmem {
     const int kp = (k + 7) & ~7;
     size_t o = 0;
     bf = o;    o += (size_t)kp * DP * 8;
-    crow = o;  o += (size_t)kp * DP * 8;
+    crow = o;  o += (size_t)kp * (DP + 1) * 8;
     chn = o;   o += (size_t)kp * 8;
     hmin = o;  o += (size_t)k * 8;
     drift = o; o += (size_t)k * 8;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 
   for (int i = tid; i < kp * DP; i += blockDim.x) {
     const int j = i / DP, e = i - j * DP;
-    crow[i] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
+    crow[j * crow_stride<DP>() + e] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
     const int l = i & 31, qs = i >> 5, q = qs / KS, s = qs - q * KS;
     const int jb = q * 8 + (l >> 2), eb = s * 4 + (l & 3);
     bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
