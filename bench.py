@@ -155,7 +155,8 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     comm = LocalComm()
-    if world > 1:
+    force_comm = os.environ.get("KNB_BENCH_FORCE_COMM") == "1"  # NCCL step loop even at N = 1
+    if world > 1 or force_comm:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         comm = TorchComm()
@@ -204,7 +205,7 @@ def run_ours(args):
     run = kb.Lloyd(dev_rows, ecfg, comm=comm, ignore_stop=True, device=local_rank)
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t_init
-    if world == 1:
+    if world == 1 and not force_comm:
         run.ctx.enqueue(args.warmup)  # iteration 0, then the graph is captured and replayed
     else:
         for _ in range(args.warmup):
@@ -216,7 +217,7 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     start.record(stream)
-    if world == 1:
+    if world == 1 and not force_comm:
         run.ctx.enqueue(args.steps)  # one CUDA graph replay per iteration
     else:
         for i in range(args.steps):
@@ -356,12 +357,25 @@ def run_ours(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or force_comm:
         torch.distributed.destroy_process_group()
     return 0
 
 
+def _json_stdout():
+    """Keep stdout for the one JSON line: anything else written to fd 1 by native code
+    (NCCL's version banner, driver messages) goes to stderr."""
+    try:
+        out = os.fdopen(os.dup(1), "w")
+        sys.stdout.flush()
+        os.dup2(2, 1)
+        sys.stdout = out
+    except OSError:  # pragma: no cover
+        pass
+
+
 def main():
+    _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
