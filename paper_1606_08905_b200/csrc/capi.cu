@@ -98,6 +98,7 @@ struct knb_ctx {
   double* partials = nullptr;  // allocated on first use by an f64 pass
   int G_alloc = 0;
   Ctrl* ctrl = nullptr;
+  unsigned int* fin_sync = nullptr;
   IterStatsDev* stats = nullptr;
   long long* bad = nullptr;
   long long* ids_dev = nullptr;
@@ -144,6 +145,7 @@ FinalArgs final_args(knb_ctx* c) {
   f.half_min = c->half_min;
   f.wterm = c->wterm;
   f.wcss_mode = c->tc ? 2 : (c->pruning ? 1 : 0);
+  f.sync = c->fin_sync;
   f.ctrl = c->ctrl;
   f.stats = c->stats;
   return f;
@@ -645,6 +647,9 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   if ((rc = dev_alloc(c, &c->wterm, k))) return bail(rc);
   if ((rc = dev_alloc(c, &c->exch, c->L))) return bail(rc);
   if ((rc = dev_alloc(c, &c->ctrl, 1))) return bail(rc);
+  if ((rc = dev_alloc(c, &c->fin_sync, 1))) return bail(rc);
+  if (cudaMemsetAsync(c->fin_sync, 0, sizeof(unsigned int), c->stream) != cudaSuccess)
+    return bail(fail(KNB_E_CUDA, "memset"));
   if ((rc = dev_alloc(c, &c->stats, max_iters))) return bail(rc);
   if ((rc = dev_alloc(c, &c->bad, 2))) return bail(rc);
   if (cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream) != cudaSuccess) return bail(fail(KNB_E_CUDA, "memset"));
@@ -660,7 +665,7 @@ int knb_destroy(knb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
-                  c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->stats,
+                  c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->fin_sync, c->stats,
                   c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
                   c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tcq, c->tcq_count, c->tc_counters, c->seg.counts,
                   c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records};

@@ -64,6 +64,7 @@ struct FinalArgs {
   double* half_min;
   double* wterm;         // k: per-centroid WCSS terms (pruned runs)
   int wcss_mode;         // 0: K1's scalar, 1: pruned formula, 2: dense from running sums
+  unsigned int* sync;    // finalize's arrival counter (reset by its last CTA)
   Ctrl* ctrl;
   IterStatsDev* stats;   // [max_iters]
 };

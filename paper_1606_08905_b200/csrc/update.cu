@@ -25,34 +25,58 @@ namespace knb {
 
 namespace {
 
+// 8 lanes per element: lane q sums CTA partials [q*S, (q+1)*S) in CTA order (S =
+// ceil(G/8), all loads in flight), then the 8 sums combine in a fixed butterfly.
 __global__ void reduce_kernel(const double* __restrict__ partials, int G, long long L,
                               double* __restrict__ out, const Ctrl* ctrl) {
   if (ctrl->stop && !ctrl->ignore_stop) return;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L;
-       e += (long long)gridDim.x * blockDim.x) {
+  const int q = threadIdx.x & 7;
+  const int S = (G + 7) / 8;
+  const int b0 = q * S, b1 = b0 + S < G ? b0 + S : G;
+  for (long long e0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3; e0 < ((L + 3) / 4) * 4;
+       e0 += ((long long)gridDim.x * blockDim.x) >> 3) {
+    const long long e = e0 < L ? e0 : L - 1;
     double s = 0.0;
-    int b = 0;
-    // four independent loads in flight, summed strictly in CTA order
-    for (; b + 4 <= G; b += 4) {
-      const double v0 = partials[(long long)b * L + e], v1 = partials[(long long)(b + 1) * L + e];
-      const double v2 = partials[(long long)(b + 2) * L + e], v3 = partials[(long long)(b + 3) * L + e];
-      s += v0;
-      s += v1;
-      s += v2;
-      s += v3;
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = partials[(long long)(b + t) * L + e];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) s += v[t];
     }
-    for (; b < G; ++b) s += partials[(long long)b * L + e];
-    out[e] = s;
+    for (; b < b1; ++b) s += partials[(long long)b * L + e];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (q == 0 && e0 < L) out[e] = s;
   }
 }
 
-// one warp per centroid
+__device__ void finalize_centroid(const FinalArgs& f, int j);
+__device__ void stats_body(const FinalArgs& f);
+__device__ void geometry_row(const FinalArgs& f, int a);
+
+// One warp per centroid; the last CTA to finish then runs the statistics row (one
+// launch instead of two; the MTI geometry stays a separate, wider kernel).
 __global__ void finalize_kernel(const FinalArgs f) {
   if (f.ctrl->stop && !f.ctrl->ignore_stop) return;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j < f.k) finalize_centroid(f, j);
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(f.sync, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  stats_body(f);
+  if (threadIdx.x == 0) *f.sync = 0u;  // ready for the next iteration (graph replays)
+}
+
+__device__ void finalize_centroid(const FinalArgs& f, int j) {
   const int k = f.k, d = f.d;
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (j >= k) return;
   const long long kd = (long long)k * d;
   double* sums = f.exch + (long long)j * d;
   double cntj = f.exch[kd + j];
@@ -110,9 +134,9 @@ __global__ void finalize_kernel(const FinalArgs f) {
   }
 }
 
-__global__ void stats_kernel(const FinalArgs f) {
+// the statistics row + convergence test, by one CTA after every centroid is final
+__device__ void stats_body(const FinalArgs& f) {
   Ctrl* c = f.ctrl;
-  if (c->stop && !c->ignore_stop) return;
   __shared__ double sw[32];
   __shared__ double sc[32];
   __shared__ double sm[32];
@@ -162,13 +186,10 @@ __global__ void stats_kernel(const FinalArgs f) {
   }
 }
 
+
 // one warp per row a of the half-distance matrix
-__global__ void geometry_kernel(const FinalArgs f) {
-  const Ctrl* c = f.ctrl;
-  if (c->stop && !c->ignore_stop) return;
+__device__ void geometry_row(const FinalArgs& f, int a) {
   const int k = f.k, d = f.d, lane = threadIdx.x & 31;
-  const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (a >= k) return;
   const double* ca = f.means + (long long)a * d;
   double mn = CUDART_INF;
   for (int b = lane; b < k; b += 32) {
@@ -186,6 +207,14 @@ __global__ void geometry_kernel(const FinalArgs f) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
   if (lane == 0) f.half_min[a] = mn;  // +inf when k == 1
+}
+
+__global__ void geometry_kernel(const FinalArgs f) {
+  const Ctrl* c = f.ctrl;
+  if (c->stop && !c->ignore_stop) return;
+  const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (a >= f.k) return;
+  geometry_row(f, a);
 }
 
 // Install initial centroids (given / forgy / kmeans++ rows, or random-partition
@@ -245,18 +274,15 @@ __global__ void cmax_kernel(const FinalArgs f) {
 
 cudaError_t launch_reduce(const double* partials, int G, long long L, double* out, const Ctrl* ctrl,
                           cudaStream_t s) {
-  long long blocks = (L + 255) / 256;
+  long long blocks = (L * 8 + 127) / 128;  // 8 lanes per element, small blocks
   if (blocks > 4096) blocks = 4096;
-  reduce_kernel<<<(int)blocks, 256, 0, s>>>(partials, G, L, out, ctrl);
+  reduce_kernel<<<(int)blocks, 128, 0, s>>>(partials, G, L, out, ctrl);
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t s) {
   const int wpb = 8;
   finalize_kernel<<<(f.k + wpb - 1) / wpb, wpb * 32, 0, s>>>(f);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  stats_kernel<<<1, 1024, 0, s>>>(f);
   return cudaGetLastError();
 }
 
