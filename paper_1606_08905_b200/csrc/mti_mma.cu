@@ -153,25 +153,38 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
     __syncwarp();
   };
 
-  // filter strided blocks (bound inflation + clause 1) until `target` survivors are queued
+  // filter strided blocks (bound inflation + clause 1) until `target` survivors are queued.
+  // The per-row state of the NEXT group of FB blocks is loaded while the current group is
+  // filtered (and across calls), so the loads' latency overlaps useful work.
   long long blk = gw;
-  // (state loads for FB blocks are issued together so their latency overlaps)
-  constexpr int FB = 4;
+  constexpr int FB = DP <= 32 ? 4 : 2;  // (DP = 64 is register-bound)
+  constexpr bool PREFETCH = DP <= 16;    // wide rows: scoring dominates, keep the registers
+  int pa[FB];
+  double pu[FB];
+  auto load_group = [&](long long b) {
+#pragma unroll
+    for (int j = 0; j < FB; ++j) {
+      const long long row = (b + j * TW) * BR + lane;
+      const bool ok = b + j * TW < nblk && row < a.n;
+      pa[j] = ok ? a.assign[row] : -1;
+      pu[j] = ok ? a.upper[row] : 0.0;
+    }
+  };
+  if constexpr (PREFETCH) load_group(blk);
   auto filter_until = [&](int target) {
     while (qn < target && blk < nblk) {
+      if constexpr (!PREFETCH) load_group(blk);
       int aa[FB];
       double uu[FB];
 #pragma unroll
-      for (int j = 0; j < FB; ++j) {
-        const long long row = (blk + j * TW) * BR + lane;
-        const bool ok = blk + j * TW < nblk && row < a.n;
-        aa[j] = ok ? a.assign[row] : -1;
-        uu[j] = ok ? a.upper[row] : 0.0;
-      }
+      for (int j = 0; j < FB; ++j) { aa[j] = pa[j]; uu[j] = pu[j]; }
+      const long long cur = blk;
+      blk += FB * TW;
+      if constexpr (PREFETCH) load_group(blk);  // prefetch the next group
 #pragma unroll
       for (int j = 0; j < FB; ++j) {
-        if (blk + j * TW >= nblk) break;  // uniform
-        const long long row = (blk + j * TW) * BR + lane;
+        if (cur + j * TW >= nblk) break;  // uniform
+        const long long row = (cur + j * TW) * BR + lane;
         bool live = false;
         if (aa[j] >= 0) {
           double u = uu[j];
@@ -192,7 +205,6 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
         }
         qn += __popc(b);
       }
-      blk += FB * TW;
       __syncwarp();
     }
   };
