@@ -154,6 +154,10 @@ int knb_get_bounds(knb_ctx* ctx, double* upper, uint8_t* tight);
 int knb_sync(knb_ctx* ctx);
 /* Benchmark hook: keep running full iterations after convergence (kmeans() never sets it). */
 int knb_set_ignore_stop(knb_ctx* ctx, int32_t on);
+/* Enqueue this context's work on `stream` from now on (NULL = the legacy default
+ * stream).  Lets a caller capture whole iterations -- local pass, its own all-reduce,
+ * finish -- into one CUDA graph on its capture stream (bench.py does at N > 1). */
+int knb_set_stream(knb_ctx* ctx, void* stream);
 /* Options.  KNB_OPT_MTI_SCAN selects how a pruned iteration re-assigns the survivors of the
  * point-skip test (clause 1): KNB_MTI_EXACT walks the candidates with clauses 2/3 exactly like
  * scan_block (pruning.py:163-204), reproducing its dist_comps / pruned_* counters;

@@ -86,6 +86,7 @@ SIGNATURES = {
     "knb_get_bounds": [_P, _P, _P],
     "knb_sync": [_P],
     "knb_set_ignore_stop": [_P, _I32],
+    "knb_set_stream": [_P, _P],
     "knb_state_bytes": [_P, _PI64],
     "knb_describe": [_P, _PI32, _PI32, _PI32, _PI32],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
@@ -331,6 +332,9 @@ class Context:
 
     def sync(self) -> None:
         check(self.L.knb_sync(self.h))
+
+    def set_stream(self, stream: int | None) -> None:
+        check(self.L.knb_set_stream(self.h, ctypes.c_void_p(stream or 0)))
 
     def set_ignore_stop(self, on: bool) -> None:
         check(self.L.knb_set_ignore_stop(self.h, int(on)))

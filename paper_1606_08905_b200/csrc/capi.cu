@@ -1158,6 +1158,20 @@ int knb_sync(knb_ctx* c) {
   return KNB_OK;
 }
 
+int knb_set_stream(knb_ctx* c, void* stream) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  KNB_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  if (c->own_stream && c->stream && c->stream != s) {
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+    cudaStreamDestroy(c->stream);
+    c->own_stream = false;
+  }
+  c->stream = s;
+  c->graph_valid = false;
+  return KNB_OK;
+}
+
 int knb_set_ignore_stop(knb_ctx* c, int32_t on) {
   if (!c) return fail(KNB_E_ARG, "null context");
   KNB_CUDA(cudaSetDevice(c->device));
