@@ -368,9 +368,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int m = 0; m < TOPK; ++m) add(hs->v[m], hs->j[m]);
           if (besti < 0 || nc > LIST || (double)dropped >= thr) {
-            flag = true;  // candidate list incomplete: all k
-            e0.y = -2;
+            // candidate list incomplete: all k, by a whole CTA (tc_rerank_full_kernel)
+            const unsigned long long pos = atomicAdd(a.counters + 3, 1ull);
+            a.fullq[pos] = (int)row;
             ++fulls;
+            ++flagged;
           } else if (nc == 1) {
             a.assign[row] = besti;
             moved += (besti != old);
@@ -416,9 +418,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 }
 
 // Exact f64 re-scoring of the rows the certificate could not settle: one warp per
-// queued row, one warp-wide exact distance per candidate (or per centroid when the
-// candidate list overflowed); the lexicographic (distance, id) minimum is the
-// reference's strict-less ascending scan (distance.py:114-116).
+// queued row, one warp-wide exact distance per candidate; the lexicographic
+// (distance, id) minimum is the reference's strict-less ascending scan
+// (distance.py:114-116).  Overflowed windows go to tc_rerank_full_kernel.
 __global__ void __launch_bounds__(128) tc_rerank_kernel(const float* __restrict__ X, int d, int k,
                                                         const double* __restrict__ means, int32_t* assign,
                                                         const int32_t* __restrict__ old_assign,
@@ -438,13 +440,40 @@ __global__ void __launch_bounds__(128) tc_rerank_kernel(const float* __restrict_
     const float* x = X + row * d;
     double bd = CUDART_INF;
     int bi = 0x7fffffff;
-    if (e0.y == -2) {
-      for (int j = 0; j < k; ++j) {
-        const double dist = sqrt(warp_exact_sq(x, means + (long long)j * d, d, lane));
-        if (dist < bd) { bd = dist; bi = j; }  // ascending, strict less
+    const int c[7] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+    if ((d & 31) == 0) {
+      // d a multiple of 32 (<= 256): the row stays in registers and every candidate's
+      // loads are independent, so all of them are in flight together
+      const int nq = d >> 5;
+      double xv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xv[q] = q < nq ? (double)x[32 * q + lane] : 0.0;
+      // candidates two at a time (the list is filled from the front); a missing second
+      // one re-reads the first centroid (L1) and is discarded
+#pragma unroll
+      for (int m = 0; m < 7; m += 2) {
+        if (c[m] < 0) break;  // warp-uniform
+        const bool two = m + 1 < 7 && c[m + 1] >= 0;
+        const double* ca = means + (long long)c[m] * d;
+        const double* cb = means + (long long)(two ? c[m + 1] : c[m]) * d;
+        double za = 0.0, zb = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < nq) {
+            const double va = __dsub_rn(xv[q], ca[32 * q + lane]);
+            const double vb = __dsub_rn(xv[q], cb[32 * q + lane]);
+            za = __fma_rn(va, va, za);
+            zb = __fma_rn(vb, vb, zb);
+          }
+        }
+        const double da = sqrt(warp_tree_finish(za, lane));
+        if (da < bd || (da == bd && c[m] < bi)) { bd = da; bi = c[m]; }
+        if (two) {
+          const double db = sqrt(warp_tree_finish(zb, lane));
+          if (db < bd || (db == bd && c[m + 1] < bi)) { bd = db; bi = c[m + 1]; }
+        }
       }
     } else {
-      const int c[7] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
 #pragma unroll
       for (int m = 0; m < 7; ++m) {
         if (c[m] >= 0) {
@@ -460,6 +489,42 @@ __global__ void __launch_bounds__(128) tc_rerank_kernel(const float* __restrict_
     }
   }
   if (lane == 0 && moved) atomicAdd(counters + 0, moved);
+}
+
+// Rows whose candidate window overflowed: every centroid, exact recipe, one CTA per row
+// (32 warps split the centroids, ascending and strict-less within a warp, then the
+// lexicographic (distance, id) minimum across warps -- the reference's scan).
+__global__ void __launch_bounds__(1024) tc_rerank_full_kernel(const float* __restrict__ X, int d, int k,
+                                                              const double* __restrict__ means, int32_t* assign,
+                                                              const int32_t* __restrict__ old_assign,
+                                                              const int* __restrict__ fullq,
+                                                              unsigned long long* counters, float* __restrict__ bound,
+                                                              const Ctrl* ctrl) {
+  if (ctrl->stop && !ctrl->ignore_stop) return;
+  __shared__ double sd[32];
+  __shared__ int si[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const long long cnt = (long long)counters[3];
+  for (long long e = blockIdx.x; e < cnt; e += gridDim.x) {
+    const long long row = fullq[e];
+    const float* x = X + row * d;
+    double bd = CUDART_INF;
+    int bi = 0x7fffffff;
+    for (int j = warp; j < k; j += nw) {
+      const double dist = sqrt(warp_exact_sq(x, means + (long long)j * d, d, lane));
+      if (dist < bd) { bd = dist; bi = j; }
+    }
+    if (lane == 0) { sd[warp] = bd; si[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w)
+        if (sd[w] < bd || (sd[w] == bd && si[w] < bi)) { bd = sd[w]; bi = si[w]; }
+      assign[row] = bi;
+      if (bi != old_assign[row]) atomicAdd(counters + 0, 1ull);
+      bound[row] = __double2float_ru(bd * (1.0 + 0x1p-40));
+    }
+    __syncthreads();
+  }
 }
 
 // f32 tensor-core operand of the centroids: k_pad x d_pad, zero padded; the score
@@ -516,6 +581,12 @@ cudaError_t launch_tc_assign(const CUtensorMap* tmX, const CUtensorMap* tmC, con
   cudaError_t e = cudaFuncSetAttribute(tc_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   tc_assign_kernel<<<grid, TC_THREADS, sm, s>>>(*tmX, *tmC, a);  // grid even: CTA pairs
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_rerank_full(const TcArgs& a, const double* means, int grid, cudaStream_t s) {
+  tc_rerank_full_kernel<<<grid, 1024, 0, s>>>(a.X, a.d, a.k, means, a.assign, a.old_assign, a.fullq, a.counters,
+                                              a.bound, a.ctrl);
   return cudaGetLastError();
 }
 

@@ -76,6 +76,7 @@ struct knb_ctx {
   float* tc_bound = nullptr;
   TcHalf* tc_scratch = nullptr;
   int4* tcq = nullptr;
+  int* tc_fullq = nullptr;
   int* tcq_count = nullptr;
   long long tcq_cap = 0;
   unsigned long long* tc_counters = nullptr;
@@ -270,6 +271,7 @@ int tc_setup(knb_ctx* c) {
   if ((rc = dev_alloc(c, &c->xn2, nl))) return rc;
   if ((rc = dev_alloc(c, &c->old_assign, nl))) return rc;
   if ((rc = dev_alloc(c, &c->tc_bound, nl))) return rc;
+  if ((rc = dev_alloc(c, &c->tc_fullq, nl))) return rc;
   if ((rc = dev_alloc(c, &c->tc_scratch, (size_t)c->G_tc * 2 * tc_rows_per_tile()))) return rc;
   if ((rc = dev_alloc(c, &c->tcq, (size_t)c->G_tc * 4 * 2 * c->tcq_cap))) return rc;
   if ((rc = dev_alloc(c, &c->tcq_count, (size_t)c->G_tc * 4))) return rc;
@@ -333,6 +335,7 @@ int tc_local(knb_ctx* c) {
   int rc = ensure_xn2(c);
   if (rc) return rc;
   KNB_CUDA(cudaMemsetAsync(c->tc_counters, 0, sizeof(unsigned long long), c->stream));
+  KNB_CUDA(cudaMemsetAsync(c->tc_counters + 3, 0, sizeof(unsigned long long), c->stream));
   KNB_CUDA(launch_tc_prep(c->means, c->cn2, c->k, c->d, c->kp, c->dp, c->c32, c->chn32, c->stream));
   TcArgs a = tc_args(c);
   if (c->n_local) {
@@ -345,6 +348,7 @@ int tc_local(knb_ctx* c) {
     }
     KNB_CUDA(launch_tc_assign(&c->tmX32, &c->tmC32, a, c->G_tc, c->stream));
     KNB_CUDA(launch_tc_rerank(a, c->means, c->G_tc * 4, c->stream));
+    KNB_CUDA(launch_tc_rerank_full(a, c->means, c->sms, c->stream));
   }
   SegArgs g = seg_args(c, c->t_host == 0 ? 0 : 1, c->assign);
   KNB_CUDA(launch_segsum(g, 4, c->stream));
@@ -376,6 +380,7 @@ TcArgs tc_args(knb_ctx* c) {
   a.bound = c->tc_bound;
   a.drift = c->drift;
   a.scratch = c->tc_scratch;
+  a.fullq = c->tc_fullq;
   return a;
 }
 
@@ -667,7 +672,7 @@ int knb_destroy(knb_ctx* c) {
   void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
                   c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->fin_sync, c->stats,
                   c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
-                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tcq, c->tcq_count, c->tc_counters, c->seg.counts,
+                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->seg.counts,
                   c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records};
   for (void* q : ptrs)
     if (q) cudaFree(q);

@@ -181,6 +181,7 @@ __device__ __forceinline__ double warp_exact_sq(const TX* __restrict__ x, const 
   double dot = 0.0;
   if (n1) {
     double z = 0.0;
+#pragma unroll 8  // independent loads: one memory latency for the whole row
     for (int i = 0; i < n32; i += 32) {
       const double v = __dsub_rn((double)x[i + lane], c[i + lane]);
       z = __fma_rn(v, v, z);
@@ -208,6 +209,20 @@ __device__ __forceinline__ double warp_exact_sq(const TX* __restrict__ x, const 
     dot = __fma_rn(v, v, dot);
   }
   return dot;
+}
+
+// The tail of warp_exact_sq for d a multiple of 32 (no 16-wide or scalar blocks):
+// lane 8a + l holds z[a][l]; returns the tree's dot in every lane.
+__device__ __forceinline__ double warp_tree_finish(double z, int lane) {
+  const double acc = __dadd_rn(z, __shfl_down_sync(0xffffffffu, z, 4));
+  const double a1 = __shfl_down_sync(0xffffffffu, acc, 8);
+  const double a2 = __shfl_down_sync(0xffffffffu, acc, 16);
+  const double a3 = __shfl_down_sync(0xffffffffu, acc, 24);
+  const double sl = __dadd_rn(__dadd_rn(__dadd_rn(acc, a1), a2), a3);
+  const double s0 = __shfl_sync(0xffffffffu, sl, 0), s1 = __shfl_sync(0xffffffffu, sl, 1);
+  const double s2 = __shfl_sync(0xffffffffu, sl, 2), s3 = __shfl_sync(0xffffffffu, sl, 3);
+  (void)lane;
+  return __dadd_rn(__dadd_rn(s0, s2), __dadd_rn(s1, s3));
 }
 
 // A zero array stand-in so exact_sq(x, Zero{}, d) computes vecdot(x, x)

@@ -87,7 +87,9 @@ struct TcArgs {
   int4* queue;           // rerank entries (2 x int4: row + up to 7 candidates), qcap per epilogue warp
   int* qcount;           // entries per epilogue warp
   long long qcap;
-  unsigned long long* counters;  // [0] reassigned this pass, [1] flagged rows, [2] full reranks (cumulative)
+  unsigned long long* counters;  // [0] reassigned this pass, [1] flagged rows, [2] full reranks (cumulative),
+                                 // [3] rows in fullq this pass
+  int* fullq;            // rows whose candidate window overflowed (re-scored against all k)
   const Ctrl* ctrl;
   double err_rel;        // certified relative error of a TF32 dot product
   float* dbg;            // non-null: dump the n x kp f32 scores instead of assigning
@@ -103,6 +105,7 @@ int tc_cols_per_tile();
 cudaError_t launch_tc_assign(const CUtensorMap* tmX, const CUtensorMap* tmC, const TcArgs& a, int grid,
                              cudaStream_t s);
 cudaError_t launch_tc_rerank(const TcArgs& a, const double* means, int regions, cudaStream_t s);
+cudaError_t launch_tc_rerank_full(const TcArgs& a, const double* means, int grid, cudaStream_t s);
 cudaError_t launch_tc_prep(const double* means, const double* cn2, int k, int d, int kp, int dp, float* c32,
                            float* chn32, cudaStream_t s);
 cudaError_t launch_row_sqnorm_f32(const float* X, long long n, int d, double* out, cudaStream_t s);
