@@ -222,14 +222,13 @@ __global__ void __launch_bounds__(KNB_NT, 1)
       // tight = 1 (scan_block's outcome); skipped rows are left exactly as the
       // reference leaves them.  A block whose rows all skip costs no tensor work.
       const int aa = valid ? old_raw : 0;
-      double u = u_pre;
       const double dr = drift_s[aa];
-      if (valid && dr != 0.0) {
-        u = u + dr;
-        a.upper[row] = u;
+      const double u = u_pre + dr;  // u + 0.0 == u
+      const bool live = valid && !(u <= hmin_s[aa]);
+      if (valid && !live && dr != 0.0) {  // a skipped row keeps the inflated bound;
+        a.upper[row] = u;                 // survivors' bounds are rewritten below
         a.tight[row] = 0;
       }
-      const bool live = valid && !(u <= hmin_s[aa]);
       skips += (valid && !live) ? 1 : 0;
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
       if (lmask) {

@@ -189,13 +189,16 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
         if (aa[j] >= 0) {
           double u = uu[j];
           const double dr = drift[aa[j]];
-          if (dr != 0.0) {  // u + 0.0 == u and tight & true == tight: no store needed
-            u = u + dr;
-            a.upper[row] = u;
-            a.tight[row] = 0;
+          u = u + dr;  // u + 0.0 == u
+          if (u <= hmin[aa[j]]) {
+            ++skips;
+            if (dr != 0.0) {  // the inflated bound is the skipped row's final state
+              a.upper[row] = u;
+              a.tight[row] = 0;
+            }
+          } else {
+            live = true;  // a survivor's bound and tight flag are rewritten by its scan
           }
-          if (u <= hmin[aa[j]]) ++skips;
-          else live = true;
         }
         const unsigned b = __ballot_sync(0xffffffffu, live);
         if (live) {
