@@ -85,3 +85,26 @@ def test_pick_owner():
     assert pick_owner([0.0, 1.0], 0.1) == (1, 0.1)
     # rounding past the end goes to the last rank holding mass
     assert pick_owner([0.3, 0.7, 0.0], 1.0 + 1e-15)[0] == 1
+
+
+def test_float32_input_routing():
+    """float32 rows stay float32 only where the tcgen05 path serves the configuration
+    (dense, 32 <= d <= 256, d % 4 == 0); everything else is upcast like check_matrix."""
+    from paper_1606_08905_b200.engine import _rows_of
+    m32 = np.ones((10, 64), dtype=np.float32)
+    host, dev = _rows_of(m32, kb.EngineConfig(k=3, pruning=False))
+    assert dev is None and host.dtype == np.float32 and host.flags.c_contiguous
+    host, _ = _rows_of(m32, kb.EngineConfig(k=3, pruning=True))
+    assert host.dtype == np.float64
+    host, _ = _rows_of(np.ones((10, 6), dtype=np.float32), kb.EngineConfig(k=3, pruning=False))
+    assert host.dtype == np.float64
+    host, _ = _rows_of(np.ones((10, 64)), kb.EngineConfig(k=3, pruning=False))
+    assert host.dtype == np.float64
+    with pytest.raises(kb.MatrixFormatError):
+        _rows_of(np.ones((0, 64), dtype=np.float32), kb.EngineConfig(k=3, pruning=False))
+
+
+def test_engine_config_scan_option_validated():
+    kb.EngineConfig(k=2, mti_scan="exact").validate()
+    with pytest.raises(ValueError, match="mti_scan"):
+        kb.EngineConfig(k=2, mti_scan="fast").validate()
