@@ -13,9 +13,15 @@ from paper_1606_08905_b200.parallel import LocalComm  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = kb.synth.CONFIGS[name]
-m = cfg["data"](cfg["n"])
-pinned = torch.empty(m.shape, dtype=torch.float64, pin_memory=True)
-pinned.copy_(torch.from_numpy(m))
+if "spec" in cfg:  # config 5: the law generated in HBM, copied to pinned host memory
+    dev = kb.synth.mixture_device(cfg["spec"](cfg["n"]))
+    pinned = torch.empty(tuple(dev.shape), dtype=dev.dtype, pin_memory=True)
+    pinned.copy_(dev)
+    del dev
+else:
+    m = cfg["data"](cfg["n"])
+    pinned = torch.empty(m.shape, dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(m))
 host = pinned.numpy()
 ec = kb.EngineConfig(k=cfg["k"], init=cfg["init"], seed=int(name[1:]), pruning=cfg["pruning"],
                      max_iters=cfg["max_iters"], tolerance=cfg["tolerance"])
@@ -26,7 +32,7 @@ for rep in range(2):
     n, d = host.shape
     ctx = _native.Context(0, n, n, 0, d, ec.k, ec.pruning, ec.max_iters, ec.tolerance, None)
     t.append(time.perf_counter())
-    ctx.upload(host)
+    (ctx.upload_f32 if host.dtype == np.float32 else ctx.upload)(host)
     t.append(time.perf_counter())
     bad = ctx.first_nonfinite_row()
     t.append(time.perf_counter())
