@@ -58,11 +58,11 @@ struct WarpSmem {
     const int NS = stages_for(DP);
     size_t o = 0;
     bf = o;   o += (size_t)kp * DP * 8;
-    crow = o; o += (size_t)kp * (DP + 1) * 8;
+    crow = o; o += (size_t)kp * (DP + 2) * 8;
     chn = o;  o += (size_t)kp * 8;
     hmin = o; o += (size_t)k * 8;
     drift = o; o += (size_t)k * 8;
-    red = o;  o += 32 * 4 * 8;
+    red = o;  o += KNB_WARPS * 8 * 8;
     o = al(o, 1024);
     warp0 = o;
     stage_bytes = (size_t)BR * DP * 8;              // multiple of 1024 for DP >= 4
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(KNB_NT, 1)
 constexpr size_t SMEM_MAX = 227 * 1024;
 
 int warps_for(int DP, int k, int d) {
-  for (int W = KNB_WARPS; W >= 1; W >>= 1)
+  for (int W = KNB_WARPS; W >= 1; --W)
     if (WarpSmem(DP, k, d, W).total <= SMEM_MAX) return W;
   return 0;
 }

@@ -15,11 +15,23 @@ namespace knb {
 
 constexpr int BR = 32;  // rows per warp block
 
-// Row stride (doubles) of the exact-recipe centroid copy in shared memory: odd, so the
-// lanes of a warp reading DIFFERENT centroids' element e hit different bank pairs
-// (a DP stride put every lane's element e in the same bank).
+// Row stride (doubles) of the exact-recipe centroid copy in shared memory: DP + 2, so
+// rows stay 16-byte aligned (16-byte loads) and the lanes of a warp reading DIFFERENT
+// centroids' chunk e spread over all eight 16-byte bank groups (a DP stride put every
+// lane in the same bank).
 template <int DP>
-__host__ __device__ constexpr int crow_stride() { return DP + 1; }
+__host__ __device__ constexpr int crow_stride() { return DP + 2; }
+
+template <int DP>
+__device__ __forceinline__ void load_crow(const double* __restrict__ crow, int j, double (&c)[DP]) {
+  const double2* p = reinterpret_cast<const double2*>(crow + j * crow_stride<DP>());
+#pragma unroll
+  for (int q = 0; q < DP / 2; ++q) {
+    const double2 v = p[q];
+    c[2 * q] = v.x;
+    c[2 * q + 1] = v.y;
+  }
+}
 
 // not volatile: the mma has no side effects, so ptxas may interleave it with the epilogue
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -224,13 +236,26 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
     double bd = CUDART_INF;
     int bi = 0;
     for (int j = 0; j < k; ++j) {
-      const double dj = sqrt(exact_sq<DP>(x, crow + j * crow_stride<DP>(), d));
+      double dj;
+      if constexpr (DP <= 32) {
+        double cj[DP];
+        load_crow<DP>(crow, j, cj);
+        dj = sqrt(exact_sq<DP>(x, cj, d));
+      } else {
+        dj = sqrt(exact_sq<DP>(x, crow + j * crow_stride<DP>(), d));
+      }
       if (dj < bd) { bd = dj; bi = j; }
     }
     id = bi;
     nd = bd;
   } else {
-    nd = sqrt(exact_sq<DP>(x, crow + id * crow_stride<DP>(), d));
+    if constexpr (DP <= 32) {  // 16-byte loads into registers
+      double ci[DP];
+      load_crow<DP>(crow, id, ci);
+      nd = sqrt(exact_sq<DP>(x, ci, d));
+    } else {  // (DP = 64 is register-bound)
+      nd = sqrt(exact_sq<DP>(x, crow + id * crow_stride<DP>(), d));
+    }
   }
   if (sq_out) *sq_out = exact_sq<DP>(x, Zero{}, d);
   return nd;

@@ -39,11 +39,11 @@ struct MtiMmaSmem {
     const int kp = (k + 7) & ~7;
     size_t o = 0;
     bf = o;    o += (size_t)kp * DP * 8;
-    crow = o;  o += (size_t)kp * (DP + 1) * 8;
+    crow = o;  o += (size_t)kp * (DP + 2) * 8;
     chn = o;   o += (size_t)kp * 8;
     hmin = o;  o += (size_t)k * 8;
     drift = o; o += (size_t)k * 8;
-    red = o;   o += 32 * 8 * 8;
+    red = o;   o += KNB_WARPS * 8 * 8;
     o = al(o, 1024);
     warp0 = o;
     size_t w = 0;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 constexpr size_t SMEM_MAX = 227 * 1024;
 
 int mti_warps_for(int DP, int k, int d) {
-  for (int W = KNB_WARPS; W >= 1; W >>= 1)
+  for (int W = KNB_WARPS; W >= 1; --W)
     if (MtiMmaSmem(DP, k, d, W).total <= SMEM_MAX) return W;
   return 0;
 }
