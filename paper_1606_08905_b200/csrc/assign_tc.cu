@@ -573,7 +573,6 @@ size_t tc_smem_bytes(int nkc) {
 }
 
 int tc_rows_per_tile() { return TC_M; }
-int tc_cols_per_tile() { return TC_N; }
 
 cudaError_t launch_tc_assign(const CUtensorMap* tmX, const CUtensorMap* tmC, const TcArgs& a, int grid,
                              cudaStream_t s) {

@@ -101,7 +101,6 @@ struct TcArgs {
 enum TcMode { TC_MAX = 0, TC_COLLECT_SMAX = 1, TC_COLLECT_BOUND = 2 };
 size_t tc_smem_bytes(int nkc);
 int tc_rows_per_tile();
-int tc_cols_per_tile();
 cudaError_t launch_tc_assign(const CUtensorMap* tmX, const CUtensorMap* tmC, const TcArgs& a, int grid,
                              cudaStream_t s);
 cudaError_t launch_tc_rerank(const TcArgs& a, const double* means, int regions, cudaStream_t s);

@@ -84,22 +84,6 @@ __device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int 
   bid = other ? oi : bid;
 }
 
-// ascending bitonic sort of one 32-bit key per lane
-__device__ __forceinline__ unsigned warp_sort(unsigned key, int lane) {
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const unsigned other = __shfl_xor_sync(0xffffffffu, key, stride);
-      const bool up = size == 32 ? true : ((lane & size) == 0);
-      const bool lower = (lane & stride) == 0;
-      const unsigned lo = key < other ? key : other, hi = key < other ? other : key;
-      key = (lower == up) ? lo : hi;
-    }
-  }
-  return key;
-}
-
 // Lane that finishes row r of a block after the quad combine (row = t4*8 + g).
 __device__ __forceinline__ int owner_lane(int r) { return ((r & 7) << 2) | (r >> 3); }
 
@@ -320,62 +304,6 @@ __device__ __forceinline__ void accumulate_in_row_order(unsigned rowmask, int to
 // Bit r set when the lane owning row r (owner_lane(r)) passes `pred`.
 __device__ __forceinline__ unsigned row_mask(bool pred, int my_row) {
   return __reduce_or_sync(0xffffffffu, pred ? (1u << my_row) : 0u);
-}
-
-// Deterministic warp-local accumulation of the block rows selected by `key`
-// (= (cluster << 5) | row for included rows, ~0 otherwise), lanes = dims:
-//   acc[c][e] += sign * sum of x[row][e] over the rows of cluster c, in row order,
-//   cnt[c] += sign * members, sqa[c] += sign * sum of sq (sq held by owner_lane(row)).
-template <int DP>
-__device__ __forceinline__ void accumulate_rows(unsigned key, double my_sq, double sign, const unsigned char* tb,
-                                                double* acc, double* cnt, double* sqa, int d, int lane) {
-  using TL = TileLayout<DP>;
-  const unsigned inc = __ballot_sync(0xffffffffu, key != 0xffffffffu);
-  if (inc == 0u) return;
-  key = warp_sort(key, lane);
-  const bool kv = key != 0xffffffffu;
-  const int kid = (int)(key >> 5);
-  const int pid = __shfl_up_sync(0xffffffffu, kid, 1);
-  const int nid = __shfl_down_sync(0xffffffffu, kid, 1);
-  const bool nv = __shfl_down_sync(0xffffffffu, (int)kv, 1) != 0;
-  const bool st = kv && (lane == 0 || pid != kid);
-  const bool en = kv && (lane == 31 || !nv || nid != kid);
-  const unsigned smask = __ballot_sync(0xffffffffu, st);
-  const unsigned emask = __ballot_sync(0xffffffffu, en);
-  const int nvalid = __popc(inc);
-  // counts and squared norms: segmented inclusive scan over the sorted positions
-  const int rr = (int)(key & 31);
-  double q = __shfl_sync(0xffffffffu, my_sq, owner_lane(rr));
-  const int head = 31 - __clz(smask & (0xffffffffu >> (31 - lane)));
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const double up = __shfl_up_sync(0xffffffffu, q, off);
-    if (lane - off >= head) q += up;
-  }
-  if (en) {
-    cnt[kid] += sign * (double)(lane - head + 1);
-    sqa[kid] += sign * q;
-  }
-  // dims: branch-free segmented sum along the sorted rows
-  const int e0 = lane < d ? lane : 0;
-  const int e1 = lane + 32 < d ? lane + 32 : 0;
-  double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-  for (int p = 0; p < 32; ++p) {
-    if (p < nvalid) {
-      const unsigned kk = __shfl_sync(0xffffffffu, key, p);
-      const int r = (int)(kk & 31);
-      const double keep = ((smask >> p) & 1u) ? 0.0 : 1.0;
-      s0 = fma(s0, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e0, BR)));
-      if constexpr (DP > 32) s1 = fma(s1, keep, *reinterpret_cast<const double*>(tb + TL::elem_off(r, e1, BR)));
-      if ((emask >> p) & 1u) {
-        const int j = (int)(kk >> 5);
-        if (lane < d) acc[j * d + lane] += sign * s0;
-        if constexpr (DP > 32)
-          if (lane + 32 < d) acc[j * d + lane + 32] += sign * s1;
-      }
-    }
-  }
 }
 
 }  // namespace knb
