@@ -30,11 +30,11 @@
 // winner's distance is recomputed with it (bit-identical to the oracle on the
 // reference's BLAS tree).
 //
-// Accumulation is warp-local and deterministic: a 15-step bitonic shuffle sort
-// orders the block's 32 rows by (cluster, row); the warp then walks the sorted
-// rows with lanes = dims, adds each cluster segment in registers and flushes it
-// into the warp's private shared-memory sums.  At the end the CTA adds its warps'
-// sums in warp order into one partial for the fixed-order reduction (update.cu).
+// Accumulation is warp-local and deterministic: the warp walks the block's rows in
+// row order with lanes = dims (accumulate_in_row_order) and adds each into its
+// private shared-memory sums -- every row on the first pass, only the moved rows'
+// signed deltas afterwards.  At the end the CTA adds its warps' sums in warp order
+// into one partial for the fixed-order reduction (update.cu).
 #include <cuda.h>
 #include <math_constants.h>
 

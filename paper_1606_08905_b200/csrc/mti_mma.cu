@@ -17,7 +17,7 @@
 // Layout: warp-independent.  A warp filters its strided 32-row blocks reading only the
 // 13 B/point state, appends survivors to a warp-private queue, and whenever 32 are
 // queued gathers their rows from HBM into a swizzled 32-row tile and scores them with
-// score_block (mma_common.cuh).  Deltas go through the warp-local sorted segment walk
+// score_block (mma_common.cuh).  Deltas go through the warp-local row-ordered walk
 // into warp-private sums; the CTA adds its warps' sums in warp order.
 #include <cuda.h>
 #include <math_constants.h>
