@@ -21,13 +21,22 @@ from .engine import (
     kmeans,
     kmeans_sharded,
 )
+from .fileio import HEADER_SIZE, MatrixIOError, load_matrix, save_matrix
 from .matrix import MatrixFormatError, RowRange, check_matrix, partition_rows
 from .parallel import LocalComm, TorchComm, shard_of
+from .report import deterministic_view, format_report, parse_report
 
 __version__ = "0.1.0"
 
 __all__ = [
     "CentroidSet",
+    "HEADER_SIZE",
+    "MatrixIOError",
+    "deterministic_view",
+    "format_report",
+    "load_matrix",
+    "parse_report",
+    "save_matrix",
     "EngineConfig",
     "INIT_METHODS",
     "IoDelta",

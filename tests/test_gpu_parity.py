@@ -252,3 +252,40 @@ def test_gpu_kmeanspp_degenerate_total_replays_reference_draws():
         o = O.lloyd(m, 3, init="kmeanspp", seed=seed, pruning=False, max_iters=3)
         np.testing.assert_array_equal(m[np.asarray(r.init_rows)], o.init_means)
         assert np.array_equal(r.centroids.means, o.means)
+
+
+@pytest.mark.parametrize("name", ["kpp_prune", "forgy_dense", "rp_prune_tol"])
+def test_gpu_cli_train_report_matches_reference_report(name, tmp_path):
+    """The command line (``train`` on a KNRM file the reference wrote) reproduces the
+    reference CLI's report: every counter of every iteration, the totals and the
+    convergence line exactly (mti_scan="exact" keeps the reference's clause-2/3
+    counters), the WCSS column to 1e-9."""
+    import os
+    from paper_1606_08905_b200.cli import main
+    from paper_1606_08905_b200.report import TIMING_FIELDS, parse_report
+    gold = os.path.join(os.path.dirname(__file__), "golden", "reports")
+    with open(os.path.join(gold, f"{name}.args")) as fh:
+        argv = fh.read().split()
+    out = tmp_path / "r.txt"
+    cwd = os.getcwd()
+    os.chdir(os.path.dirname(os.path.dirname(__file__)))
+    try:
+        assert main(["train", "--data", f"tests/golden/reports/{name}.knrm", *argv, "--mti-scan", "exact",
+                     "--report", str(out)]) == 0
+    finally:
+        os.chdir(cwd)
+    ours = parse_report(out.read_text())
+    with open(os.path.join(gold, f"{name}.report")) as fh:
+        ref = parse_report(fh.read())
+    assert ours["config"] == ref["config"] and ours["converged"] == ref["converged"]
+    assert len(ours["iterations"]) == len(ref["iterations"])
+    for a, b in zip(ours["iterations"], ref["iterations"]):
+        for key in a:
+            if key in TIMING_FIELDS:
+                continue
+            if key == "wcss":
+                assert abs(a[key] - b[key]) <= 1e-9 * abs(b[key]), (key, a, b)
+            else:
+                assert a[key] == b[key], (key, a, b)
+    assert {k: v for k, v in ours["totals"].items() if k not in TIMING_FIELDS} == \
+        {k: v for k, v in ref["totals"].items() if k not in TIMING_FIELDS}
