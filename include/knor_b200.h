@@ -66,6 +66,12 @@ int knb_destroy(knb_ctx* ctx);
  * buffer, or attach caller-owned device rows.  Replaces _MemorySource (engine.py:162-191). */
 int knb_upload_rows(knb_ctx* ctx, const double* host, int64_t row_lo_local, int64_t rows);
 int knb_attach_rows(knb_ctx* ctx, const double* dev_rows);
+/* Rows that stay in host memory (larger than HBM): the caller's array is page-locked and
+ * mapped (cudaHostRegister) and every kernel reads it over the host link; clause-1
+ * skipped rows of a pruned pass are never fetched -- the B200 form of the reference's
+ * semi-external mode with row elision (outofcore.py:163-225, §8(f) f2).  The array must
+ * outlive the context (unregistered by knb_destroy). */
+int knb_attach_host_rows(knb_ctx* ctx, const double* host_rows);
 /* f32 rows (BASELINE config 5), kept as f32 in HBM -- the reference upcasts them to f64
  * (matrix.py:40), which is exact, and every result here equals the f64 upcast's.  Only the
  * dense tensor-core path takes them: knb_f32_supported(d, k, pruning) says whether it

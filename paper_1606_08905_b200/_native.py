@@ -55,6 +55,7 @@ SIGNATURES = {
     "knb_destroy": [_P],
     "knb_upload_rows": [_P, _P, _I64, _I64],
     "knb_attach_rows": [_P, _P],
+    "knb_attach_host_rows": [_P, _P],
     "knb_upload_rows_f32": [_P, _P, _I64, _I64],
     "knb_attach_rows_f32": [_P, _P],
     "knb_tc_info": [_P, _PI32, _PI64, _PI64],
@@ -183,6 +184,20 @@ class Context:
 
     def attach(self, dev_ptr: int) -> None:
         check(self.L.knb_attach_rows(self.h, ctypes.c_void_p(dev_ptr)))
+
+    def attach_host(self, rows: np.ndarray) -> None:
+        """Rows stay in host memory (page-locked + mapped) and are read over the host link.
+        A file mapping the driver cannot lock (np.memmap) is first read into anonymous
+        memory -- still no HBM copy."""
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        try:
+            check(self.L.knb_attach_host_rows(self.h, ptr(rows)))
+        except RuntimeError:
+            if not isinstance(rows, np.memmap) and rows.base is None:
+                raise
+            rows = np.array(rows, dtype=np.float64, order="C")
+            check(self.L.knb_attach_host_rows(self.h, ptr(rows)))
+        self._host_rows = rows  # the registered buffer lives as long as the context
 
     def upload_f32(self, rows: np.ndarray, lo: int = 0) -> None:
         """f32 rows for the tensor-core path (see f32_supported)."""

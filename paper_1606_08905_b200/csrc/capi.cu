@@ -59,6 +59,7 @@ struct knb_ctx {
 
   const double* X = nullptr;
   double* X_own = nullptr;
+  const void* host_registered = nullptr;  // knb_attach_host_rows: pinned + mapped caller rows
   CUtensorMap tmap;
   int use_tma = 0;
 
@@ -169,6 +170,7 @@ int reset_run(knb_ctx* c) {
 
 int build_tmap(knb_ctx* c) {
   c->use_tma = 0;
+  if (c->host_registered) return KNB_OK;  // rows in host memory: cp.async gathers, no tensor maps
   if (c->DP == 0 || (c->d & 1) || (reinterpret_cast<uintptr_t>(c->X) & 15) || c->n_local < 1 ||
       c->n_local > 0x7fffffffLL)
     return KNB_OK;
@@ -678,6 +680,7 @@ int knb_destroy(knb_ctx* c) {
     if (q) cudaFree(q);
   if (c->own_exch && c->exch) cudaFree(c->exch);
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->host_registered) cudaHostUnregister(const_cast<void*>(c->host_registered));
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -757,6 +760,34 @@ int knb_upload_rows(knb_ctx* c, const double* host, int64_t lo, int64_t rows) {
     KNB_CUDA(cudaMemcpyAsync(c->X_own + lo * c->d, host, sizeof(double) * rows * c->d, cudaMemcpyHostToDevice,
                              c->stream));
   return KNB_OK;
+}
+
+int knb_attach_host_rows(knb_ctx* c, const double* host) {
+  if (!c || (!host && c->n_local > 0)) return fail(KNB_E_ARG, "null argument");
+  if (c->tc) return fail(KNB_E_STATE, "context holds f32 rows");
+  KNB_CUDA(cudaSetDevice(c->device));
+  if (c->host_registered) {
+    cudaHostUnregister(const_cast<void*>(c->host_registered));
+    c->host_registered = nullptr;
+  }
+  if (c->n_local == 0) return KNB_OK;
+  const size_t bytes = sizeof(double) * (size_t)c->n_local * c->d;
+  void* p = const_cast<double*>(host);
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    e = cudaHostRegister(p, bytes, cudaHostRegisterMapped);  // read-only registration is optional
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // not sticky: keep it out of the next launch check
+    return fail(KNB_E_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  }
+  c->host_registered = host;
+  void* dptr = nullptr;
+  KNB_CUDA(cudaHostGetDevicePointer(&dptr, p, 0));
+  c->X = static_cast<const double*>(dptr);
+  c->graph_valid = false;
+  return build_tmap(c);
 }
 
 int knb_attach_rows(knb_ctx* c, const double* dev) {

@@ -47,6 +47,11 @@ class EngineConfig:
     counters), "dense" scores survivors on the FP64 tensor cores (same
     assignments, bounds, skips and centroids; dist_comps = k per survivor,
     pruned_* = 0), "auto" = "dense" where the tensor-core kernel applies.
+    ``host_rows``: a host array is not copied to HBM but page-locked and read over
+    the host link by every pass (data larger than HBM); pruned passes fetch only
+    the survivors of clause 1, and each iteration reports its link traffic in
+    ``IterationStats.io`` (rows_elided = skipped rows), like the reference's
+    semi-external mode.
     """
 
     k: int
@@ -66,6 +71,7 @@ class EngineConfig:
     device: int | None = None
     batch: int = 16
     mti_scan: str = "auto"
+    host_rows: bool = False
 
     def validate(self) -> None:
         if self.k < 1:
@@ -174,7 +180,7 @@ def _rows_of(matrix, cfg: EngineConfig):
         is_tensor = False
 
     def keep_f32(dtype_is_f32, d):
-        return dtype_is_f32 and _native.f32_supported(d, cfg.k, cfg.pruning)
+        return dtype_is_f32 and not cfg.host_rows and _native.f32_supported(d, cfg.k, cfg.pruning)
 
     if is_tensor:
         import torch
@@ -194,13 +200,35 @@ def _rows_of(matrix, cfg: EngineConfig):
     return check_shape(a), None
 
 
-def _attach_rows(ctx, host, dev) -> None:
+def _apply_options(ctx, cfg: EngineConfig) -> None:
+    if cfg.mti_scan != "auto":
+        ctx.set_option(_native.KNB_OPT_MTI_SCAN, _native.MTI_SCAN[cfg.mti_scan])
+    elif cfg.host_rows and cfg.pruning:
+        try:  # compacted survivors: skipped rows never cross the host link
+            ctx.set_option(_native.KNB_OPT_MTI_SCAN, _native.MTI_SCAN["dense"])
+        except ValueError:
+            pass
+
+
+def _attach_rows(ctx, host, dev, host_rows: bool = False) -> None:
     if dev is not None:
         (ctx.attach_f32 if dev.element_size() == 4 else ctx.attach)(dev.data_ptr())
     elif host.dtype == np.float32:
         ctx.upload_f32(host)
+    elif host_rows:
+        ctx.attach_host(host)
     else:
         ctx.upload(host)
+
+
+def _link_io(stats, k: int, d: int) -> list[IoDelta]:
+    """Host-row runs: bytes fetched over the link per iteration (rows scored x row bytes)
+    and the rows clause 1 kept off the link."""
+    out = []
+    for s in stats:
+        b = (int(s.dist_comps) // max(k, 1)) * d * 8
+        out.append(IoDelta(bytes_requested=b, bytes_read=b, rows_elided=int(s.skips)))
+    return out
 
 
 def kmeans(matrix, cfg: EngineConfig) -> KmeansResult:
@@ -250,12 +278,11 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
     cls = context_cls or _native.Context
     ctx = cls(device, n, n_local, row_lo, d, k, cfg.pruning, cfg.max_iters, cfg.tolerance, stream)
     try:
-        if cfg.mti_scan != "auto":
-            ctx.set_option(_native.KNB_OPT_MTI_SCAN, _native.MTI_SCAN[cfg.mti_scan])
+        _apply_options(ctx, cfg)
         exch = comm.make_exchange(ctx.exchange_len(), device)
         if exch is not None:
             ctx.set_exchange(exch.data_ptr(), exch.numel())
-        _attach_rows(ctx, host, dev)
+        _attach_rows(ctx, host, dev, cfg.host_rows)
         bad = ctx.first_nonfinite_row()
         bad_global = comm.allreduce_min_int(row_lo + bad if bad >= 0 else n)
         if bad_global < n:
@@ -297,11 +324,17 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         if state["count_error"]:
             raise RuntimeError(f"accumulator counts sum to a value other than {n}")
         means, prev, counts, drift = ctx.centroids()
+        io = _link_io(rows_stats, k, d) if (cfg.host_rows and host is not None) else [None] * len(rows_stats)
         its = [IterationStats(t=int(s.t), reassignments=int(s.reassignments), wcss=float(s.wcss),
                               dist_comps=int(s.dist_comps), skips=int(s.skips),
                               pruned_stale=int(s.pruned_stale), pruned_tight=int(s.pruned_tight),
-                              wall_s=walls[i] if i < len(walls) else 0.0)
+                              wall_s=walls[i] if i < len(walls) else 0.0, io=io[i])
                for i, s in enumerate(rows_stats)]
+        io_totals = None
+        if io and io[0] is not None:
+            io_totals = IoDelta(bytes_requested=sum(x.bytes_requested for x in io),
+                                bytes_read=sum(x.bytes_read for x in io),
+                                rows_elided=sum(x.rows_elided for x in io))
         assignments = ctx.assignments()
         peak = ctx.state_bytes()
         return KmeansResult(
@@ -309,7 +342,7 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
             assignments=assignments,
             iterations=its,
             converged=bool(state["converged"]),
-            io_totals=None,
+            io_totals=io_totals,
             peak_state_bytes=peak,
             assignment_history=history,
             row_lo=row_lo,
@@ -343,13 +376,12 @@ class Lloyd:
             stream = torch_stream(device)
         self.ctx = _native.Context(device, self.n, self.n_local, self.row_lo, self.d, cfg.k, cfg.pruning,
                                    cfg.max_iters, cfg.tolerance, stream)
-        if cfg.mti_scan != "auto":
-            self.ctx.set_option(_native.KNB_OPT_MTI_SCAN, _native.MTI_SCAN[cfg.mti_scan])
+        _apply_options(self.ctx, cfg)
         self._dev = dev
         self.exch = self.comm.make_exchange(self.ctx.exchange_len(), device)
         if self.exch is not None:
             self.ctx.set_exchange(self.exch.data_ptr(), self.exch.numel())
-        _attach_rows(self.ctx, host, dev)
+        _attach_rows(self.ctx, host, dev, cfg.host_rows)
         self.init_rows = device_init(self.ctx, self.comm, self.exch, cfg.init, cfg.k, cfg.seed,
                                      cfg.initial_centroids, self.n, self.row_lo, self.n_local, self.d)
         if ignore_stop:

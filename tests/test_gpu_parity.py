@@ -289,3 +289,38 @@ def test_gpu_cli_train_report_matches_reference_report(name, tmp_path):
                 assert a[key] == b[key], (key, a, b)
     assert {k: v for k, v in ours["totals"].items() if k not in TIMING_FIELDS} == \
         {k: v for k, v in ref["totals"].items() if k not in TIMING_FIELDS}
+
+
+@pytest.mark.parametrize("pruning", [True, False])
+def test_gpu_host_rows_equal_hbm_rows(pruning, tmp_path):
+    """Rows left in host memory (page-locked, read over the link; here a memory-mapped
+    KNRM file): identical results to the HBM copy, and per-iteration link traffic with
+    the clause-1 skipped rows elided."""
+    from paper_1606_08905_b200.fileio import load_matrix, save_matrix
+    m = kb.synth.mixture(kb.synth.MixtureSpec(40000, 12, 16, 9, "uniform", -5, 5, 0.7))
+    path = tmp_path / "x.knrm"
+    save_matrix(m, path)
+    cfg = dict(k=16, init="kmeanspp", seed=9, pruning=pruning, max_iters=12)
+    a = kb.kmeans(m, kb.EngineConfig(**cfg))
+    b = kb.kmeans(load_matrix(path, check_finite=False), kb.EngineConfig(host_rows=True, **cfg))
+    assert a.n_iterations == b.n_iterations
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids.means, b.centroids.means)
+    row = 12 * 8
+    assert b.iterations[0].io.bytes_read == 40000 * row
+    for s in b.iterations:
+        assert s.io.rows_elided == s.skips
+        assert s.io.bytes_read == (s.dist_comps // 16) * row
+    if pruning:
+        assert b.io_totals.rows_elided > 0
+        assert b.io_totals.bytes_read < b.n_iterations * 40000 * row
+
+
+def test_gpu_host_rows_plain_array():
+    m = kb.synth.uniform(30000, 8, 5)
+    cfg = dict(k=7, init="forgy", seed=5, pruning=True, max_iters=8)
+    a = kb.kmeans(m, kb.EngineConfig(**cfg))
+    b = kb.kmeans(m, kb.EngineConfig(host_rows=True, **cfg))
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids.means, b.centroids.means)
+    assert b.io_totals is not None and a.io_totals is None
