@@ -439,6 +439,7 @@ int launch_local(knb_ctx* c) {
   m.partials = c->partials;
   m.ctrl = c->ctrl;
   m.half_in_smem = c->half_in_smem;
+  m.row_gather = c->host_registered ? 1 : 0;
   m.gate = 0;
   const int mode = c->mti_mma_ok ? c->mti_scan : KNB_MTI_EXACT;
   if (mode == KNB_MTI_EXACT) {

@@ -46,6 +46,7 @@ struct MtiArgs {
   double* partials;
   const Ctrl* ctrl;
   int half_in_smem;
+  int row_gather;          // rows in host memory: the warp fetches one row per request
 };
 
 struct FinalArgs {

@@ -113,17 +113,27 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 
   // async gather of queued entries [base, base + cnum) into a staging tile (rows 0..cnum-1)
   auto gather = [&](unsigned char* dst, int base, int cnum) {
-    if (lane < cnum) {
-      const double* src = a.X + (long long)qrow[base + lane] * d;
-      if (vec) {
+    if (vec && !a.row_gather) {
+      // HBM rows: every lane copies its own row (unrolled, no index arithmetic)
+      if (lane < cnum) {
+        const double* src = a.X + (long long)qrow[base + lane] * d;
 #pragma unroll
         for (int q2 = 0; q2 < DP / 2; ++q2)
           if (2 * q2 < d) cp_async16(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
-      } else {
-#pragma unroll
-        for (int e = 0; e < DP; ++e)
-          if (e < d) cp_async8(dst + TL::elem_off(lane, e, BR), src + e);
       }
+    } else if (vec) {
+      // consecutive lanes copy consecutive 16-byte chunks of the same row: each row
+      // is fetched as one coalesced request (matters most for rows in host memory)
+      const int hd = d >> 1;
+      for (int i = lane; i < cnum * hd; i += 32) {
+        const int r = i / hd, q2 = i - r * hd;
+        cp_async16(dst + TL::chunk_off(r, q2, BR), a.X + (long long)qrow[base + r] * d + 2 * q2);
+      }
+    } else if (lane < cnum) {
+      const double* src = a.X + (long long)qrow[base + lane] * d;
+#pragma unroll
+      for (int e = 0; e < DP; ++e)
+        if (e < d) cp_async8(dst + TL::elem_off(lane, e, BR), src + e);
     }
     cp_async_commit();
   };
