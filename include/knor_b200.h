@@ -72,6 +72,27 @@ int knb_attach_rows(knb_ctx* ctx, const double* dev_rows);
  * semi-external mode with row elision (outofcore.py:163-225, §8(f) f2).  The array must
  * outlive the context (unregistered by knb_destroy). */
 int knb_attach_host_rows(knb_ctx* ctx, const double* host_rows);
+/* Semi-external run (kmeans_ondisk, outofcore.py:440-455; _DiskSource :293-355): from now
+ * on every iteration (1) marks the rows the reference would fetch -- all rows on a full
+ * pass (task_rows), the survivors of clause 1 on a pruned pass (rows_by_ids) -- and keeps
+ * the reference's I/O counters for it exactly (fetch_rows, :163-225: bytes requested, cache
+ * hits/misses against the published cache, page_size x distinct pages of each task's
+ * uncached rows), and (2) at the refresh iterations start, 3 start, 7 start, ...
+ * (should_refresh, :282-290) rebuilds an HBM row cache like RowCache.rebuild (:250-270):
+ * each of the T worker partitions keeps its smallest (capacity / T) / row_bytes fetched row
+ * ids.  Pruned passes over host rows gather cached rows from HBM instead of the host link.
+ * One GPU holding the whole matrix (n_local == n_global), f64 rows; call before the
+ * centroids are installed.  Same argument errors as the reference (T, task_size,
+ * page_size >= 1, capacity >= 0, refresh start >= 1). */
+int knb_sem_configure(knb_ctx* ctx, int32_t T, int64_t task_size, int64_t page_size,
+                      int32_t cache_enabled, int64_t cache_capacity, int32_t refresh_start);
+/* Per-iteration IoDelta (engine.py:112-118) of the first `count` iterations, 5 int64 per
+ * iteration: bytes_requested, bytes_read, cache_hits, cache_misses, rows fetched
+ * (rows_elided is the iteration's skips). */
+int knb_sem_io(knb_ctx* ctx, int64_t* out, int32_t count);
+/* The published cache: row ids (slot order: partition, then ascending id) and, if rows is
+ * non-null, their cached values (cap x d); *count = cached rows (may exceed cap). */
+int knb_sem_cache(knb_ctx* ctx, int64_t* ids, double* rows, int64_t cap, int64_t* count);
 /* f32 rows (BASELINE config 5), kept as f32 in HBM -- the reference upcasts them to f64
  * (matrix.py:40), which is exact, and every result here equals the f64 upcast's.  Only the
  * dense tensor-core path takes them: knb_f32_supported(d, k, pruning) says whether it

@@ -86,3 +86,45 @@ def case_cfg(name: str) -> dict:
     if "initial" in cfg:
         cfg["initial"] = np.asarray(cfg["initial"], dtype=np.float64)
     return cfg
+
+
+# Semi-external runs (kmeans_ondisk, outofcore.py:440-455): data law, EngineConfig
+# fields (mode="sem"), and the kmeans_ondisk keywords.  page_size is the RowStore's.
+SEM_CASES = {
+    "sem_nocache": dict(data=lambda: mixture(MixtureSpec(1600, 8, 4, 19, "uniform", -50, 50, 1.0)),
+                        cfg=dict(k=4, seed=3, T=2, max_iters=40),
+                        io=dict(cache_enabled=False)),
+    "sem_zero_cap": dict(data=lambda: uniform(1500, 6, 3),
+                         cfg=dict(k=4, seed=2, T=2, max_iters=40),
+                         io=dict(cache_capacity=0, start=1)),
+    "sem_quarter": dict(data=lambda: mixture(MixtureSpec(20000, 8, 8, 61, "uniform", -4, 4, 1.0)),
+                        cfg=dict(k=8, seed=13, T=2, max_iters=40),
+                        io=dict(cache_capacity=20000 * 64 // 4, start=5)),
+    "sem_full_s2": dict(data=lambda: uniform(6000, 8, 3),
+                        cfg=dict(k=6, seed=2, T=2, max_iters=40),
+                        io=dict(cache_capacity=6000 * 64, start=2)),
+    "sem_plain_cache": dict(data=lambda: mixture(MixtureSpec(4000, 8, 6, 7, "uniform", -3, 3, 1.0)),
+                            cfg=dict(k=6, seed=2, T=3, max_iters=11, pruning=False),
+                            io=dict(cache_capacity=4000 * 64 // 2, start=2)),
+    "sem_tasks_pages": dict(data=lambda: mixture(MixtureSpec(5000, 8, 7, 23, "uniform", -2, 2, 1.0)),
+                            cfg=dict(k=7, seed=4, T=3, task_size=100, max_iters=40),
+                            io=dict(cache_capacity=5000 * 64 // 4, start=1, page_size=1000)),
+    "sem_wide_rows": dict(data=lambda: uniform(1200, 300, 8),
+                          cfg=dict(k=5, seed=1, T=2, max_iters=30),
+                          io=dict(cache_capacity=1200 * 2400 // 3, start=2)),
+    "sem_kpp_d3": dict(data=lambda: mixture(MixtureSpec(7000, 3, 9, 5, "uniform", -8, 8, 1.0)),
+                       cfg=dict(k=9, seed=5, T=4, task_size=333, init="kmeanspp", max_iters=40),
+                       io=dict(cache_capacity=7000 * 24 // 10, start=1, page_size=512)),
+    "sem_d1": dict(data=lambda: mixture(MixtureSpec(5000, 1, 5, 31, "uniform", -20, 20, 1.0)),
+                   cfg=dict(k=5, seed=31, T=1, max_iters=30),
+                   io=dict(cache_capacity=5000 * 8 // 4, start=3)),
+}
+
+
+def sem_case(name: str):
+    """(matrix, EngineConfig kwargs, kmeans_ondisk kwargs, page_size, refresh start)."""
+    c = SEM_CASES[name]
+    io = dict(c["io"])
+    page = io.pop("page_size", 4096)
+    start = io.pop("start", 5)
+    return c["data"](), dict(c["cfg"]), io, page, start

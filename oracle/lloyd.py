@@ -257,6 +257,7 @@ class OracleResult:
     init_means: np.ndarray | None = None
     upper: np.ndarray | None = None
     tight: np.ndarray | None = None
+    fetched: list[np.ndarray] | None = None  # collect_fetch: rows each iteration reads
 
     @property
     def n_iterations(self) -> int:
@@ -356,7 +357,8 @@ class _Run:
 def lloyd(m, k: int, *, max_iters: int = 100, init: str = "forgy", seed: int = 0,
           pruning: bool = True, tolerance: float = 0, initial=None, T: int = 1,
           task_size: int = 8192, collect: bool = False, threads: int | None = None,
-          init_override: np.ndarray | None = None, force_iters: bool = False) -> OracleResult:
+          init_override: np.ndarray | None = None, force_iters: bool = False,
+          collect_fetch: bool = False) -> OracleResult:
     """The in-memory engine end to end (engine.py:211-500), sequential-equivalent.
 
     ``T``/``task_size`` fix the accumulator granularity exactly as the reference
@@ -364,6 +366,9 @@ def lloyd(m, k: int, *, max_iters: int = 100, init: str = "forgy", seed: int = 0
     how many host threads run the blocks.  ``init_override`` skips the RNG init
     and starts from the given means (used by the sampled step-wise oracle);
     ``force_iters`` keeps iterating after convergence (benchmark arm only).
+    ``collect_fetch`` records, per iteration, the rows a semi-external run reads:
+    every row on a full pass (task_rows), the clause-1 survivors on a pruned pass
+    (rows_by_ids, engine.py:321-334) -- the input of oracle/outofcore.py.
     """
     m = as_matrix(m)
     n, d = m.shape
@@ -383,12 +388,16 @@ def lloyd(m, k: int, *, max_iters: int = 100, init: str = "forgy", seed: int = 0
     pool = ThreadPoolExecutor(max_workers=workers) if workers > 1 else None
     its: list[OracleIteration] = []
     hist = [] if collect else None
+    fetched = [] if collect_fetch else None
     converged = False
     full = True
     t = 0
     try:
         while True:
             t_start = time.perf_counter()
+            if fetched is not None:
+                fetched.append(np.ones(n, dtype=bool) if full else
+                               ~(run.upper <= run.half_min[run.assign]))
             fn = run.full_block if full else run.pruned_block
             if pool is None:
                 parts = [fn(lo, hi) for lo, hi in blocks]
@@ -442,7 +451,7 @@ def lloyd(m, k: int, *, max_iters: int = 100, init: str = "forgy", seed: int = 0
             pool.shutdown()
     return OracleResult(means=run.means, prev_means=prev, counts=counts, drift=drift,
                         assignments=run.assign.copy(), iterations=its, converged=converged,
-                        history=hist, init_means=means0,
+                        history=hist, init_means=means0, fetched=fetched,
                         upper=None if run.upper is None else run.upper.copy(),
                         tight=None if run.tight is None else run.tight.copy())
 

@@ -23,13 +23,18 @@ from .engine import (
 )
 from .fileio import HEADER_SIZE, MatrixIOError, load_matrix, save_matrix
 from .matrix import MatrixFormatError, RowRange, check_matrix, partition_rows
+from .outofcore import CacheSchedule, RowStore, kmeans_ondisk, should_refresh
 from .parallel import LocalComm, TorchComm, shard_of
 from .report import deterministic_view, format_report, parse_report
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "CacheSchedule",
     "CentroidSet",
+    "RowStore",
+    "kmeans_ondisk",
+    "should_refresh",
     "HEADER_SIZE",
     "MatrixIOError",
     "deterministic_view",

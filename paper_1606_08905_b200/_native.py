@@ -56,6 +56,9 @@ SIGNATURES = {
     "knb_upload_rows": [_P, _P, _I64, _I64],
     "knb_attach_rows": [_P, _P],
     "knb_attach_host_rows": [_P, _P],
+    "knb_sem_configure": [_P, _I32, _I64, _I64, _I32, _I64, _I32],
+    "knb_sem_io": [_P, _PI64, _I32],
+    "knb_sem_cache": [_P, _PI64, _P, _I64, _PI64],
     "knb_upload_rows_f32": [_P, _P, _I64, _I64],
     "knb_attach_rows_f32": [_P, _P],
     "knb_tc_info": [_P, _PI32, _PI64, _PI64],
@@ -198,6 +201,28 @@ class Context:
             rows = np.array(rows, dtype=np.float64, order="C")
             check(self.L.knb_attach_host_rows(self.h, ptr(rows)))
         self._host_rows = rows  # the registered buffer lives as long as the context
+
+    def sem_configure(self, T: int, task_size: int, page_size: int, cache_enabled: bool,
+                      cache_capacity: int, refresh_start: int) -> None:
+        check(self.L.knb_sem_configure(self.h, T, task_size, page_size, 1 if cache_enabled else 0,
+                                       cache_capacity, refresh_start))
+
+    def sem_io(self, count: int) -> np.ndarray:
+        """(count, 5) int64: bytes_requested, bytes_read, cache_hits, cache_misses, rows."""
+        out = np.zeros((max(count, 1), 5), dtype=np.int64)
+        check(self.L.knb_sem_io(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), count))
+        return out[:count]
+
+    def sem_cache(self, with_rows: bool = True):
+        """(ids, rows) of the published HBM row cache."""
+        cnt = ctypes.c_int64()
+        check(self.L.knb_sem_cache(self.h, None, None, 0, ctypes.byref(cnt)))
+        m = cnt.value
+        ids = np.zeros(max(m, 1), dtype=np.int64)
+        rows = np.zeros((max(m, 1), self.d), dtype=np.float64) if with_rows else None
+        check(self.L.knb_sem_cache(self.h, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                   ptr(rows) if with_rows else None, m, ctypes.byref(cnt)))
+        return ids[:m], (rows[:m] if with_rows else None)
 
     def upload_f32(self, rows: np.ndarray, lo: int = 0) -> None:
         """f32 rows for the tensor-core path (see f32_supported)."""

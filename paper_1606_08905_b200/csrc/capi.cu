@@ -111,6 +111,11 @@ struct knb_ctx {
   long long* kpp_idx = nullptr;
   int kpp_nblk = 0;
 
+  // semi-external runs (knb_sem_configure): I/O accounting + HBM row cache (sem.cu)
+  bool sem = false;
+  SemArgs semA;
+  int sem_nb = 0;
+
   long long t_host = 0;
   bool centroids_set = false;
   long long bytes = 0;
@@ -164,6 +169,10 @@ int reset_run(knb_ctx* c) {
   KNB_CUDA(cudaMemsetAsync(c->assign, 0, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
   KNB_CUDA(cudaMemsetAsync(c->run, 0, sizeof(double) * c->L, c->stream));
   if (c->tc_counters) KNB_CUDA(cudaMemsetAsync(c->tc_counters, 0, 4 * sizeof(unsigned long long), c->stream));
+  if (c->sem) {  // a new run starts with an empty cache and zero I/O counters
+    KNB_CUDA(cudaMemsetAsync(c->semA.io, 0, sizeof(long long) * 4 * c->max_iters, c->stream));
+    KNB_CUDA(cudaMemsetAsync(c->semA.cslot, 0xff, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
+  }
   c->t_host = 0;
   return KNB_OK;
 }
@@ -410,7 +419,32 @@ DenseArgs dense_args(knb_ctx* c) {
   return a;
 }
 
+int launch_pass(knb_ctx* c);
+
+SemArgs sem_args(knb_ctx* c) {
+  SemArgs s = c->semA;
+  s.assign = c->assign;
+  s.upper = c->upper;
+  s.drift = c->drift;
+  s.half_min = c->half_min;
+  s.X = c->X;
+  s.ctrl = c->ctrl;
+  return s;
+}
+
+// one iteration's local work; semi-external runs add the I/O accounting before the
+// pass (it needs the bounds the pass overwrites) and the cache refresh after it
 int launch_local(knb_ctx* c) {
+  if (!c->sem) return launch_pass(c);
+  const SemArgs s = sem_args(c);
+  KNB_CUDA(launch_sem_account(s, c->sms, c->stream));
+  int rc = launch_pass(c);
+  if (rc) return rc;
+  KNB_CUDA(launch_sem_rebuild(s, c->sms, c->stream));
+  return KNB_OK;
+}
+
+int launch_pass(knb_ctx* c) {
   if (c->tc) return tc_local(c);
   int rc = ensure_partials(c);
   if (rc) return rc;
@@ -440,6 +474,8 @@ int launch_local(knb_ctx* c) {
   m.ctrl = c->ctrl;
   m.half_in_smem = c->half_in_smem;
   m.row_gather = c->host_registered ? 1 : 0;
+  m.cslot = (c->sem && c->host_registered && c->semA.rows_per_part > 0) ? c->semA.cslot : nullptr;
+  m.cache = c->semA.cache;
   m.gate = 0;
   const int mode = c->mti_mma_ok ? c->mti_scan : KNB_MTI_EXACT;
   if (mode == KNB_MTI_EXACT) {
@@ -581,6 +617,7 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   std::memset(&c->tmX32, 0, sizeof(c->tmX32));
   std::memset(&c->tmC32, 0, sizeof(c->tmC32));
   std::memset(&c->seg, 0, sizeof(c->seg));
+  std::memset(&c->semA, 0, sizeof(c->semA));
   c->device = device;
   c->n_global = n_global;
   c->n_local = n_local;
@@ -676,7 +713,9 @@ int knb_destroy(knb_ctx* c) {
                   c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->fin_sync, c->stats,
                   c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
                   c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->seg.counts,
-                  c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records};
+                  c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records,
+                  c->semA.fetched, c->semA.cslot, c->semA.crow, c->semA.cache, c->semA.bcount, c->semA.bpre,
+                  c->semA.plo, c->semA.io};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (c->own_exch && c->exch) cudaFree(c->exch);
@@ -1102,6 +1141,98 @@ int knb_enqueue(knb_ctx* c, int32_t count) {
   if (rc) return rc;
   for (int b = 0; b < count && c->t_host < c->max_iters; ++b)
     if ((rc = enqueue_iteration(c))) return rc;
+  return KNB_OK;
+}
+
+int knb_sem_configure(knb_ctx* c, int32_t T, int64_t task_size, int64_t page_size, int32_t cache_enabled,
+                      int64_t cache_capacity, int32_t refresh_start) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (c->sem) return fail(KNB_E_STATE, "semi-external accounting already configured");
+  if (c->n_local != c->n_global) return fail(KNB_E_ARG, "semi-external runs use one GPU (the whole matrix)");
+  if (c->elem != 8) return fail(KNB_E_ARG, "semi-external runs read f64 rows");
+  if (T < 1) return fail(KNB_E_ARG, "T must be >= 1");
+  if (task_size < 1) return fail(KNB_E_ARG, "task_size must be >= 1");
+  if (page_size < 1) return fail(KNB_E_ARG, "page_size must be >= 1");
+  if (cache_capacity < 0) return fail(KNB_E_ARG, "capacity must be >= 0");
+  if (refresh_start < 1) return fail(KNB_E_ARG, "refresh start must be >= 1");
+  KNB_CUDA(cudaSetDevice(c->device));
+  SemArgs& s = c->semA;
+  s.n = c->n_local;
+  s.d = c->d;
+  s.T = T;
+  s.pruning = c->pruning;
+  s.cache_enabled = cache_enabled ? 1 : 0;
+  s.refresh_start = refresh_start;
+  s.max_iters = c->max_iters;
+  s.task_size = task_size;
+  s.page_size = page_size;
+  s.row_bytes = 8LL * c->d;
+  s.pbase = c->n_local / T;
+  s.prem = c->n_local % T;
+  s.rows_per_part = cache_enabled ? (cache_capacity / T) / s.row_bytes : 0;  // RowCache.__init__
+  const long long n = c->n_local;
+  int rc;
+  c->sem_nb = sem_rebuild_blocks(n);
+  if ((rc = dev_alloc(c, &s.fetched, n))) return rc;
+  if ((rc = dev_alloc(c, &s.cslot, n))) return rc;
+  if ((rc = dev_alloc(c, &s.io, 4 * (size_t)c->max_iters))) return rc;
+  if (s.rows_per_part > 0) {
+    const size_t slots = (size_t)T * s.rows_per_part;
+    if ((rc = dev_alloc(c, &s.crow, slots))) return rc;
+    if ((rc = dev_alloc(c, &s.cache, slots * c->d))) return rc;
+    if ((rc = dev_alloc(c, &s.bcount, c->sem_nb))) return rc;
+    if ((rc = dev_alloc(c, &s.bpre, c->sem_nb))) return rc;
+    if ((rc = dev_alloc(c, &s.plo, T))) return rc;
+    KNB_CUDA(cudaMemsetAsync(s.crow, 0xff, sizeof(long long) * slots, c->stream));
+  }
+  KNB_CUDA(cudaMemsetAsync(s.cslot, 0xff, sizeof(int32_t) * n, c->stream));
+  KNB_CUDA(cudaMemsetAsync(s.io, 0, sizeof(long long) * 4 * c->max_iters, c->stream));
+  c->sem = true;
+  c->graph_valid = false;
+  return KNB_OK;
+}
+
+int knb_sem_io(knb_ctx* c, int64_t* out, int32_t count) {
+  if (!c || !out) return fail(KNB_E_ARG, "null argument");
+  if (!c->sem) return fail(KNB_E_STATE, "no semi-external accounting configured");
+  if (count < 0 || count > c->max_iters) return fail(KNB_E_ARG, "count outside [0, max_iters]");
+  std::vector<long long> h(4 * (size_t)(count ? count : 1));
+  KNB_CUDA(cudaMemcpyAsync(h.data(), c->semA.io, sizeof(long long) * 4 * count, cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  const SemArgs& s = c->semA;
+  for (int i = 0; i < count; ++i) {
+    out[5 * i + 0] = h[4 * i + 0] * s.row_bytes;   // bytes_requested
+    out[5 * i + 1] = h[4 * i + 1] * s.page_size;   // bytes_read
+    out[5 * i + 2] = h[4 * i + 2];                 // cache_hits
+    out[5 * i + 3] = h[4 * i + 3];                 // cache_misses
+    out[5 * i + 4] = h[4 * i + 0];                 // rows fetched
+  }
+  return KNB_OK;
+}
+
+int knb_sem_cache(knb_ctx* c, int64_t* ids, double* rows, int64_t cap, int64_t* count) {
+  if (!c || !count) return fail(KNB_E_ARG, "null argument");
+  if (!c->sem) return fail(KNB_E_STATE, "no semi-external accounting configured");
+  const SemArgs& s = c->semA;
+  const long long slots = (long long)s.T * s.rows_per_part;
+  *count = 0;
+  if (slots == 0) return KNB_OK;
+  std::vector<long long> crow(slots);
+  KNB_CUDA(cudaMemcpyAsync(crow.data(), s.crow, sizeof(long long) * slots, cudaMemcpyDeviceToHost, c->stream));
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  long long m = 0;
+  for (long long j = 0; j < slots; ++j) {
+    if (crow[j] < 0) continue;
+    if (m < cap) {
+      if (ids) ids[m] = crow[j];
+      if (rows)
+        KNB_CUDA(cudaMemcpyAsync(rows + m * s.d, s.cache + j * s.d, sizeof(double) * s.d, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    }
+    ++m;
+  }
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
+  *count = m;
   return KNB_OK;
 }
 

@@ -47,7 +47,36 @@ struct MtiArgs {
   const Ctrl* ctrl;
   int half_in_smem;
   int row_gather;          // rows in host memory: the warp fetches one row per request
+  const int32_t* cslot;    // semi-external runs: HBM cache slot per row (-1: read X), or null
+  const double* cache;     // [slots][d]
 };
+
+// semi-external I/O accounting + HBM row cache (sem.cu)
+struct SemArgs {
+  long long n;
+  int d, T, pruning, cache_enabled, refresh_start;
+  long long max_iters;
+  long long task_size, page_size, row_bytes;
+  long long pbase, prem;       // partition_rows: n / T, n % T
+  long long rows_per_part;     // (capacity / T) / row_bytes
+  const int32_t* assign;
+  const double* upper;
+  const double* drift;
+  const double* half_min;
+  const double* X;             // rows (host-mapped or HBM)
+  uint8_t* fetched;            // [n] rows fetched by the current iteration
+  int32_t* cslot;              // [n] cache slot or -1
+  long long* crow;             // [slots] row id or -1
+  double* cache;               // [slots][d]
+  long long* bcount;           // [rebuild blocks]
+  long long* bpre;             // [rebuild blocks]
+  long long* plo;              // [T]
+  long long* io;               // [max_iters][4]: rows requested, pages read, hits, misses
+  const Ctrl* ctrl;
+};
+int sem_rebuild_blocks(long long n);
+cudaError_t launch_sem_account(const SemArgs& s, int sms, cudaStream_t st);
+cudaError_t launch_sem_rebuild(const SemArgs& s, int sms, cudaStream_t st);
 
 struct FinalArgs {
   int k, d;

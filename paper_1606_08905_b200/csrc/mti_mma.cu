@@ -121,19 +121,30 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
         for (int q2 = 0; q2 < DP / 2; ++q2)
           if (2 * q2 < d) cp_async16(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
       }
-    } else if (vec) {
-      // consecutive lanes copy consecutive 16-byte chunks of the same row: each row
-      // is fetched as one coalesced request (matters most for rows in host memory)
-      const int hd = d >> 1;
-      for (int i = lane; i < cnum * hd; i += 32) {
-        const int r = i / hd, q2 = i - r * hd;
-        cp_async16(dst + TL::chunk_off(r, q2, BR), a.X + (long long)qrow[base + r] * d + 2 * q2);
+    } else {
+      // rows in host memory (or in the HBM row cache of a semi-external run)
+      const double* src = nullptr;
+      if (lane < cnum) {
+        const int r = qrow[base + lane];
+        const int slot = a.cslot ? a.cslot[r] : -1;
+        src = slot >= 0 ? a.cache + (long long)slot * d : a.X + (long long)r * d;
       }
-    } else if (lane < cnum) {
-      const double* src = a.X + (long long)qrow[base + lane] * d;
+      if (vec) {
+        // consecutive lanes copy consecutive 16-byte chunks of the same row: each
+        // row is fetched as one coalesced request over the host link
+        const int hd = d >> 1, tot = cnum * hd;
+        for (int i0 = 0; i0 < tot; i0 += 32) {
+          const int i = i0 + lane;
+          const int r = (i < tot ? i : tot - 1) / hd, q2 = i - r * hd;
+          const double* p = reinterpret_cast<const double*>(
+              __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), r));
+          if (i < tot) cp_async16(dst + TL::chunk_off(r, q2, BR), p + 2 * q2);
+        }
+      } else if (lane < cnum) {
 #pragma unroll
-      for (int e = 0; e < DP; ++e)
-        if (e < d) cp_async8(dst + TL::elem_off(lane, e, BR), src + e);
+        for (int e = 0; e < DP; ++e)
+          if (e < d) cp_async8(dst + TL::elem_off(lane, e, BR), src + e);
+      }
     }
     cp_async_commit();
   };

@@ -151,6 +151,7 @@ class KmeansResult:
     assignment_history: list[np.ndarray] | None = None
     row_lo: int = 0
     init_rows: list[int] | None = None
+    row_cache: tuple | None = None  # kmeans_ondisk(inspect_cache=True): (ids, rows) of the HBM cache
 
     @property
     def n_iterations(self) -> int:
@@ -261,7 +262,15 @@ def kmeans_sharded(local_rows, cfg: EngineConfig, comm, n_global: int | None = N
     return _run(host, dev, cfg, comm, device=device, n_global=n_global, context_cls=context_cls)
 
 
-def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context_cls=None) -> KmeansResult:
+def _run_sem(host_rows: np.ndarray, cfg: EngineConfig, sem: dict) -> KmeansResult:
+    """kmeans_ondisk's engine run (outofcore.py): one GPU, rows in host memory, the
+    reference's I/O accounting and HBM row cache configured on the context."""
+    host, _ = _rows_of(host_rows, cfg)
+    return _run(host, None, cfg, LocalComm(), device=cfg.device, sem=sem)
+
+
+def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context_cls=None,
+         sem: dict | None = None) -> KmeansResult:
     rows = host if host is not None else dev
     n_local, d = int(rows.shape[0]), int(rows.shape[1])
     sizes = comm.allgather_int(n_local)
@@ -279,6 +288,11 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
     ctx = cls(device, n, n_local, row_lo, d, k, cfg.pruning, cfg.max_iters, cfg.tolerance, stream)
     try:
         _apply_options(ctx, cfg)
+        inspect_cache = False
+        if sem is not None:
+            sem = dict(sem)
+            inspect_cache = bool(sem.pop("inspect_cache", False))
+            ctx.sem_configure(**sem)
         exch = comm.make_exchange(ctx.exchange_len(), device)
         if exch is not None:
             ctx.set_exchange(exch.data_ptr(), exch.numel())
@@ -324,7 +338,14 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         if state["count_error"]:
             raise RuntimeError(f"accumulator counts sum to a value other than {n}")
         means, prev, counts, drift = ctx.centroids()
-        io = _link_io(rows_stats, k, d) if (cfg.host_rows and host is not None) else [None] * len(rows_stats)
+        if sem is not None:
+            raw = ctx.sem_io(len(rows_stats))
+            io = [IoDelta(bytes_requested=int(r[0]), bytes_read=int(r[1]), cache_hits=int(r[2]),
+                          cache_misses=int(r[3]), rows_elided=int(s.skips)) for r, s in zip(raw, rows_stats)]
+        elif cfg.host_rows and host is not None:
+            io = _link_io(rows_stats, k, d)
+        else:
+            io = [None] * len(rows_stats)
         its = [IterationStats(t=int(s.t), reassignments=int(s.reassignments), wcss=float(s.wcss),
                               dist_comps=int(s.dist_comps), skips=int(s.skips),
                               pruned_stale=int(s.pruned_stale), pruned_tight=int(s.pruned_tight),
@@ -334,7 +355,10 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         if io and io[0] is not None:
             io_totals = IoDelta(bytes_requested=sum(x.bytes_requested for x in io),
                                 bytes_read=sum(x.bytes_read for x in io),
+                                cache_hits=sum(x.cache_hits for x in io),
+                                cache_misses=sum(x.cache_misses for x in io),
                                 rows_elided=sum(x.rows_elided for x in io))
+        row_cache = ctx.sem_cache() if inspect_cache else None
         assignments = ctx.assignments()
         peak = ctx.state_bytes()
         return KmeansResult(
@@ -347,6 +371,7 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
             assignment_history=history,
             row_lo=row_lo,
             init_rows=init_rows,
+            row_cache=row_cache,
         )
     finally:
         ctx.close()

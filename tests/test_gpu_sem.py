@@ -1,0 +1,99 @@
+"""§8(f) f2 on the GPU: kmeans_ondisk (rows in host memory, HBM row cache) against the
+reference's own semi-external runs (tests/golden/sem/): identical assignments every
+iteration, identical per-iteration I/O counters (bytes requested, page-granular bytes
+read, cache hits / misses, rows elided), identical published cache with bit-exact
+cached rows; and equal to the in-memory engine."""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_1606_08905_b200 as kb
+from conftest import CENTROID_RTOL, ROOT
+from oracle import lloyd as O
+from oracle import outofcore as OC
+from oracle.golden_cases import SEM_CASES, sem_case
+from paper_1606_08905_b200.outofcore import CacheSchedule, RowStore, kmeans_ondisk
+
+pytestmark = pytest.mark.gpu
+SEM_GOLD = os.path.join(ROOT, "tests", "golden", "sem")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int32).tobytes()).hexdigest()
+
+
+def _io(res):
+    return np.array([[s.io.bytes_requested, s.io.bytes_read, s.io.cache_hits, s.io.cache_misses,
+                      s.io.rows_elided] for s in res.iterations], dtype=np.int64)
+
+
+def _run(tmp_path, name, collect=True, **over):
+    m, cfg, io, page, start = sem_case(name)
+    path = tmp_path / f"{name}.raw"
+    m.tofile(path)
+    cfg.update(over)
+    with RowStore(path, *m.shape, page_size=page) as store:
+        res = kmeans_ondisk(store, kb.EngineConfig(mode="sem", collect_assignments=collect, **cfg),
+                            schedule=CacheSchedule(start), inspect_cache=True, **io)
+    return m, res
+
+
+@pytest.mark.parametrize("name", list(SEM_CASES))
+def test_sem_matches_reference_golden(tmp_path, name):
+    g = np.load(os.path.join(SEM_GOLD, f"{name}.npz"))
+    m, res = _run(tmp_path, name)
+    assert [_sha(h) for h in res.assignment_history] == list(g["history_sha"])
+    assert np.array_equal(_io(res), g["io"])
+    tot = res.io_totals
+    assert [tot.bytes_requested, tot.bytes_read, tot.cache_hits, tot.cache_misses, tot.rows_elided] == \
+        list(g["io"].sum(axis=0))
+    ids, rows = res.row_cache
+    assert np.array_equal(np.sort(ids), g["cached_ids"])
+    assert rows.tobytes() == m[ids].tobytes()  # cached rows bit-identical to the file's
+    scale = max(1.0, float(np.abs(g["means"]).max()))
+    assert float(np.abs(res.centroids.means - g["means"]).max()) <= CENTROID_RTOL * scale
+    assert bool(res.converged) == bool(g["converged"])
+
+
+@pytest.mark.parametrize("name", ["sem_quarter", "sem_tasks_pages", "sem_plain_cache", "sem_kpp_d3"])
+def test_sem_graph_replay_equals_stepwise(tmp_path, name):
+    """Without a history the run is batched (CUDA-graph replay); same counters."""
+    g = np.load(os.path.join(SEM_GOLD, f"{name}.npz"))
+    _, res = _run(tmp_path, name, collect=False)
+    assert np.array_equal(_io(res), g["io"])
+    assert [s.reassignments for s in res.iterations] == list(g["reassignments"])
+
+
+def test_sem_exact_scan_same_counters(tmp_path):
+    g = np.load(os.path.join(SEM_GOLD, "sem_quarter.npz"))
+    _, res = _run(tmp_path, "sem_quarter", mti_scan="exact")
+    assert np.array_equal(_io(res), g["io"])
+    assert [_sha(h) for h in res.assignment_history] == list(g["history_sha"])
+
+
+def test_sem_equals_in_memory_any_capacity(tmp_path):
+    m = kb.synth.mixture(kb.synth.MixtureSpec(30000, 16, 12, 4, "uniform", -3, 3, 1.0))
+    path = tmp_path / "m.knrm"
+    kb.save_matrix(m, path)
+    base = dict(k=12, seed=6, T=4, max_iters=60, collect_assignments=True)
+    im = kb.kmeans(m, kb.EngineConfig(**base))
+    data_bytes = m.nbytes
+    o = O.lloyd(m, 12, seed=6, max_iters=60, T=4, collect_fetch=True)
+    for cap in (0, data_bytes // 4, data_bytes):
+        with RowStore.open(path) as store:
+            sem = kmeans_ondisk(store, kb.EngineConfig(mode="sem", **base), cache_capacity=cap,
+                                schedule=CacheSchedule(2))
+        assert sem.n_iterations == im.n_iterations
+        for a, b in zip(sem.assignment_history, im.assignment_history):
+            assert np.array_equal(a, b)
+        assert np.array_equal(sem.centroids.means, im.centroids.means)
+        want = OC.io_counters(o.fetched, [s.skips for s in o.iterations], 30000, 16, 4, 8192, 4096, True, cap, 2)
+        assert np.array_equal(_io(sem), want)
+        if cap == data_bytes:  # everything active after the first refresh is served from HBM
+            post = [s for s in sem.iterations if s.t > 2]
+            assert post and all(s.io.cache_misses == 0 for s in post)
