@@ -35,7 +35,8 @@ __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / 
 struct MtiMmaSmem {
   size_t bf, crow, chn, hmin, drift, red, warp0, tile_off, tile_stride, q_off, acc_off, cnt_off, sq_off, per_warp,
       total;
-  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W) {
+  // src: semi-external runs also queue each row's HBM cache slot
+  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W, bool src = false) {
     const int kp = (k + 7) & ~7;
     size_t o = 0;
     bf = o;    o += (size_t)kp * DP * 8;
@@ -49,7 +50,7 @@ struct MtiMmaSmem {
     size_t w = 0;
     tile_stride = (size_t)BR * DP * 8;
     tile_off = w; w += 2 * tile_stride;  // two staging tiles (gather double buffer)
-    q_off = w;    w += 192 * 4 * 2;      // queued rows and their pre-scan assignment
+    q_off = w;    w += 192 * 4 * (src ? 3 : 2);  // queued rows, pre-scan assignment (, cache slot)
     acc_off = w;  w += (size_t)k * d * 8;
     cnt_off = w;  w += (size_t)k * 8;
     sq_off = w;   w += (size_t)k * 8;
@@ -58,7 +59,9 @@ struct MtiMmaSmem {
   }
 };
 
-template <int DP>
+// HOST: rows in host memory (row_gather) and/or the semi-external HBM row cache; the
+// HBM-resident instantiation keeps the plain per-lane gather
+template <int DP, bool HOST>
 __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;
@@ -69,7 +72,8 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   const int W = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
-  const MtiMmaSmem L(DP, k, d, W);
+  const int32_t* cslot = HOST ? a.cslot : nullptr;
+  const MtiMmaSmem L(DP, k, d, W, cslot != nullptr);
   double* bf = reinterpret_cast<double*>(smem + L.bf);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
   double* chn = reinterpret_cast<double*>(smem + L.chn);
@@ -80,6 +84,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   unsigned char* tb = wbase + L.tile_off;
   int* qrow = reinterpret_cast<int*>(wbase + L.q_off);
   int* qorig = qrow + 192;
+  int* qsrc = qrow + 384;  // semi-external runs: the row's HBM cache slot (-1: host memory)
   double* acc = reinterpret_cast<double*>(wbase + L.acc_off);
   double* cnt = reinterpret_cast<double*>(wbase + L.cnt_off);
   double* sqa = reinterpret_cast<double*>(wbase + L.sq_off);
@@ -113,22 +118,24 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 
   // async gather of queued entries [base, base + cnum) into a staging tile (rows 0..cnum-1)
   auto gather = [&](unsigned char* dst, int base, int cnum) {
-    if (vec && !a.row_gather) {
-      // HBM rows: every lane copies its own row (unrolled, no index arithmetic)
+    // source of each lane's row: HBM rows, the HBM row cache (semi-external runs), or
+    // host memory
+    const double* src = nullptr;
+    bool host = false;
+    if (lane < cnum) {
+      const int r = qrow[base + lane];
+      const int slot = cslot ? qsrc[base + lane] : -1;
+      src = slot >= 0 ? a.cache + (long long)slot * d : a.X + (long long)r * d;
+      host = a.row_gather && slot < 0;
+    }
+    if (vec && (!HOST || !__any_sync(0xffffffffu, host))) {
+      // rows in HBM: every lane copies its own row (unrolled, no index arithmetic)
       if (lane < cnum) {
-        const double* src = a.X + (long long)qrow[base + lane] * d;
 #pragma unroll
         for (int q2 = 0; q2 < DP / 2; ++q2)
           if (2 * q2 < d) cp_async16(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
       }
     } else {
-      // rows in host memory (or in the HBM row cache of a semi-external run)
-      const double* src = nullptr;
-      if (lane < cnum) {
-        const int r = qrow[base + lane];
-        const int slot = a.cslot ? a.cslot[r] : -1;
-        src = slot >= 0 ? a.cache + (long long)slot * d : a.X + (long long)r * d;
-      }
       if (vec) {
         // consecutive lanes copy consecutive 16-byte chunks of the same row: each
         // row is fetched as one coalesced request over the host link
@@ -180,7 +187,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   long long blk = gw;
   constexpr int FB = DP <= 32 ? 4 : 2;  // (DP = 64 is register-bound)
   constexpr bool PREFETCH = DP <= 16;    // wide rows: scoring dominates, keep the registers
-  int pa[FB];
+  int pa[FB], ps[FB];
   double pu[FB];
   auto load_group = [&](long long b) {
 #pragma unroll
@@ -189,16 +196,21 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
       const bool ok = b + j * TW < nblk && row < a.n;
       pa[j] = ok ? a.assign[row] : -1;
       pu[j] = ok ? a.upper[row] : 0.0;
+      if constexpr (HOST) ps[j] = (ok && cslot) ? cslot[row] : -1;
     }
   };
   if constexpr (PREFETCH) load_group(blk);
   auto filter_until = [&](int target) {
     while (qn < target && blk < nblk) {
       if constexpr (!PREFETCH) load_group(blk);
-      int aa[FB];
+      int aa[FB], sl[FB];
       double uu[FB];
 #pragma unroll
-      for (int j = 0; j < FB; ++j) { aa[j] = pa[j]; uu[j] = pu[j]; }
+      for (int j = 0; j < FB; ++j) {
+        aa[j] = pa[j];
+        uu[j] = pu[j];
+        if constexpr (HOST) sl[j] = ps[j];
+      }
       const long long cur = blk;
       blk += FB * TW;
       if constexpr (PREFETCH) load_group(blk);  // prefetch the next group
@@ -226,6 +238,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
           const int pos = qn + __popc(b & ((1u << lane) - 1u));
           qrow[pos] = (int)row;
           qorig[pos] = aa[j];
+          if (HOST && cslot) qsrc[pos] = sl[j];
         }
         qn += __popc(b);
       }
@@ -253,10 +266,18 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
     // pop the processed batch from the queue
     const int rest = qn - b0;
     for (int i0 = 0; i0 < rest; i0 += 32) {
-      int rr = 0, ro = 0;
-      if (i0 + lane < rest) { rr = qrow[b0 + i0 + lane]; ro = qorig[b0 + i0 + lane]; }
+      int rr = 0, ro = 0, rs = 0;
+      if (i0 + lane < rest) {
+        rr = qrow[b0 + i0 + lane];
+        ro = qorig[b0 + i0 + lane];
+        if (HOST && cslot) rs = qsrc[b0 + i0 + lane];
+      }
       __syncwarp();
-      if (i0 + lane < rest) { qrow[i0 + lane] = rr; qorig[i0 + lane] = ro; }
+      if (i0 + lane < rest) {
+        qrow[i0 + lane] = rr;
+        qorig[i0 + lane] = ro;
+        if (HOST && cslot) qsrc[i0 + lane] = rs;
+      }
       __syncwarp();
     }
     qn = rest;
@@ -294,21 +315,28 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 
 constexpr size_t SMEM_MAX = 227 * 1024;
 
-int mti_warps_for(int DP, int k, int d) {
+int mti_warps_for(int DP, int k, int d, bool src = false) {
   for (int W = KNB_WARPS; W >= 1; --W)
-    if (MtiMmaSmem(DP, k, d, W).total <= SMEM_MAX) return W;
+    if (MtiMmaSmem(DP, k, d, W, src).total <= SMEM_MAX) return W;
   return 0;
+}
+
+template <int DP, bool HOST>
+cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
+  const bool src = HOST && a.cslot != nullptr;
+  const int W = mti_warps_for(DP, a.k, a.d, src);
+  if (!W) return cudaErrorInvalidValue;
+  const MtiMmaSmem L(DP, a.k, a.d, W, src);
+  cudaError_t e =
+      cudaFuncSetAttribute(mti_mma_kernel<DP, HOST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return e;
+  mti_mma_kernel<DP, HOST><<<grid, W * 32, L.total, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <int DP>
 cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
-  const int W = mti_warps_for(DP, a.k, a.d);
-  if (!W) return cudaErrorInvalidValue;
-  const MtiMmaSmem L(DP, a.k, a.d, W);
-  cudaError_t e = cudaFuncSetAttribute(mti_mma_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-  if (e != cudaSuccess) return e;
-  mti_mma_kernel<DP><<<grid, W * 32, L.total, s>>>(a);
-  return cudaGetLastError();
+  return (a.row_gather || a.cslot) ? launch_host<DP, true>(a, grid, s) : launch_host<DP, false>(a, grid, s);
 }
 
 }  // namespace

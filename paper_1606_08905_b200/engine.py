@@ -383,7 +383,7 @@ class Lloyd:
     ``comm`` each rank passes its own row shard, as in ``kmeans_sharded``."""
 
     def __init__(self, rows, cfg: EngineConfig, comm=None, ignore_stop: bool = False,
-                 device: int | None = None):
+                 device: int | None = None, sem: dict | None = None):
         cfg.validate()
         self.comm = comm or LocalComm()
         host, dev = _rows_of(rows, cfg)
@@ -402,6 +402,8 @@ class Lloyd:
         self.ctx = _native.Context(device, self.n, self.n_local, self.row_lo, self.d, cfg.k, cfg.pruning,
                                    cfg.max_iters, cfg.tolerance, stream)
         _apply_options(self.ctx, cfg)
+        if sem is not None:  # semi-external accounting + HBM row cache (knb_sem_configure)
+            self.ctx.sem_configure(**sem)
         self._dev = dev
         self.exch = self.comm.make_exchange(self.ctx.exchange_len(), device)
         if self.exch is not None:
