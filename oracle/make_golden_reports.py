@@ -21,6 +21,13 @@ CASES = {
     "kpp_prune": (3000, 6, 9, ["--init", "kmeanspp", "--seed", "4"]),
     "forgy_dense": (2500, 4, 7, ["--init", "forgy", "--seed", "2", "--no-prune"]),
     "rp_prune_tol": (2000, 3, 5, ["--init", "random-partition", "--seed", "1", "--tolerance", "3"]),
+    # semi-external runs (outofcore.py): the report carries the I/O counters
+    "sem_cache": (3000, 6, 9, ["--mode", "sem", "--seed", "4", "-T", "2", "--refresh-start", "2",
+                               "--cache-capacity", "48000"]),
+    "sem_nocache_pages": (2000, 5, 6, ["--mode", "sem", "--no-cache", "--page-size", "1000",
+                                       "--task-size", "300", "-T", "3", "--seed", "3"]),
+    "sem_plain": (2500, 4, 7, ["--mode", "sem", "--no-prune", "--seed", "2", "--refresh-start", "1",
+                               "--cache-capacity", "20000"]),
 }
 
 
@@ -28,7 +35,9 @@ def main() -> None:
     sys.path.insert(0, REF)
     from numakmeans.matrix import save_matrix  # reference writer: the format under test
     os.makedirs(OUT, exist_ok=True)
-    for name, (n, d, k, extra) in CASES.items():
+    names = sys.argv[1:] or list(CASES)
+    for name in names:
+        n, d, k, extra = CASES[name]
         rng = np.random.default_rng(100 + n)
         centers = rng.uniform(-6, 6, (k, d))
         x = centers[rng.integers(0, k, n)] + rng.standard_normal((n, d))

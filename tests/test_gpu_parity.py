@@ -254,12 +254,14 @@ def test_gpu_kmeanspp_degenerate_total_replays_reference_draws():
         assert np.array_equal(r.centroids.means, o.means)
 
 
-@pytest.mark.parametrize("name", ["kpp_prune", "forgy_dense", "rp_prune_tol"])
+@pytest.mark.parametrize("name", ["kpp_prune", "forgy_dense", "rp_prune_tol", "sem_cache", "sem_nocache_pages",
+                                  "sem_plain"])
 def test_gpu_cli_train_report_matches_reference_report(name, tmp_path):
     """The command line (``train`` on a KNRM file the reference wrote) reproduces the
     reference CLI's report: every counter of every iteration, the totals and the
     convergence line exactly (mti_scan="exact" keeps the reference's clause-2/3
-    counters), the WCSS column to 1e-9."""
+    counters), the WCSS column to 1e-9; ``--mode sem`` runs add the reference's I/O
+    columns (bytes requested / read, cache hits / misses, rows elided), also exact."""
     import os
     from paper_1606_08905_b200.cli import main
     from paper_1606_08905_b200.report import TIMING_FIELDS, parse_report

@@ -14,26 +14,20 @@ import pytest
 import paper_1606_08905_b200 as kb
 from conftest import ROOT
 from oracle import lloyd as O
-from paper_1606_08905_b200.cli import build_parser
-from paper_1606_08905_b200.engine import IterationStats, KmeansResult
+from oracle import outofcore as OC
+from paper_1606_08905_b200.cli import build_parser, config_echo
+from paper_1606_08905_b200.engine import IoDelta, IterationStats, KmeansResult
 from paper_1606_08905_b200.fileio import HEADER_SIZE, load_matrix, read_header, save_matrix
 from paper_1606_08905_b200.report import deterministic_view, format_report, parse_report
 
 GOLD = os.path.join(ROOT, "tests", "golden", "reports")
-NAMES = ["kpp_prune", "forgy_dense", "rp_prune_tol"]
+NAMES = ["kpp_prune", "forgy_dense", "rp_prune_tol", "sem_cache", "sem_nocache_pages", "sem_plain"]
 
 
 def _args(name):
     with open(os.path.join(GOLD, f"{name}.args")) as fh:
         argv = fh.read().split()
     return build_parser().parse_args(["train", "--data", f"tests/golden/reports/{name}.knrm", *argv])
-
-
-def _echo(a):
-    return {"data": a.data, "k": a.k, "mode": a.mode, "pruning": a.prune, "cache": None, "scheduler": a.scheduler,
-            "T": a.threads, "N": a.nodes, "task_size": a.task_size, "max_iters": a.max_iters, "init": a.init,
-            "seed": a.seed, "tolerance": a.tolerance, "page_size": None, "cache_capacity": None,
-            "refresh_start": None}
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -50,13 +44,20 @@ def test_reference_written_files_load(name):
 def test_report_of_oracle_run_equals_reference_report(name):
     a = _args(name)
     m = np.asarray(load_matrix(os.path.join(ROOT, a.data)))
-    o = O.lloyd(m, a.k, init=a.init, seed=a.seed, pruning=a.prune, tolerance=a.tolerance, max_iters=a.max_iters)
+    o = O.lloyd(m, a.k, init=a.init, seed=a.seed, pruning=a.prune, tolerance=a.tolerance, max_iters=a.max_iters,
+                T=a.threads, task_size=a.task_size, collect_fetch=True)
+    io = [None] * len(o.iterations)
+    if a.mode == "sem":  # the reference's I/O accounting, restated by oracle/outofcore.py
+        enabled = True if a.cache is None else a.cache
+        cnt = OC.io_counters(o.fetched, [s.skips for s in o.iterations], *m.shape, a.threads, a.task_size,
+                             a.page_size, enabled, a.cache_capacity, a.refresh_start)
+        io = [IoDelta(*map(int, r)) for r in cnt]
     res = KmeansResult(centroids=None, assignments=o.assignments, converged=o.converged,
                        iterations=[IterationStats(t=s.t, reassignments=s.reassignments, wcss=s.wcss,
                                                   dist_comps=s.dist_comps, skips=s.skips,
                                                   pruned_stale=s.pruned_stale, pruned_tight=s.pruned_tight,
-                                                  wall_s=s.wall_s) for s in o.iterations])
-    ours = format_report(_echo(a), res)
+                                                  wall_s=s.wall_s, io=io[i]) for i, s in enumerate(o.iterations)])
+    ours = format_report(config_echo(a), res)
     with open(os.path.join(GOLD, f"{name}.report")) as fh:
         ref = fh.read()
     assert deterministic_view(ours) == deterministic_view(ref)
@@ -102,5 +103,5 @@ def test_cli_info_and_gen(tmp_path, capsys):
     assert main(["info", str(out)]) == 0
     text = capsys.readouterr().out
     assert "n 100" in text and "d 3" in text and f"file_bytes {HEADER_SIZE + 2400}" in text
-    with pytest.raises(SystemExit, match="sem"):
-        main(["train", "--data", str(out), "--k", "2", "--mode", "sem"])
+    with pytest.raises(SystemExit, match="sem mode only"):
+        main(["train", "--data", str(out), "--k", "2", "--cache"])
