@@ -19,8 +19,65 @@ namespace knb {
 // ---------------------------------------------------------------- exact recipe
 // x: the point, either in registers (natural order) or any addressable array;
 // c: the centroid row.  d <= DP.  Mirrors oracle/exact_tree.c::tree_sq.
+// exact_sq for d == DP: the tree's shape is known at compile time (no per-element
+// bound tests -- for d = 32 those were a fifth of the MTI kernel's instructions)
+template <int DP, typename XS, typename CS>
+__device__ __forceinline__ double exact_sq_fixed(const XS& x, const CS& c) {
+  constexpr int n1 = DP & ~15, n32 = n1 & ~31;
+  double dot = 0.0;
+  if constexpr (n1 > 0) {
+    double acc[4][4];
+    if constexpr (n32 > 0) {
+      double z[4][8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) z[a][l] = 0.0;
+#pragma unroll
+      for (int i = 0; i < n32; i += 32)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int l = 0; l < 8; ++l) {
+            const double v = __dsub_rn(x[i + 8 * a + l], c[i + 8 * a + l]);
+            z[a][l] = __fma_rn(v, v, z[a][l]);
+          }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[a][l] = __dadd_rn(z[a][l], z[a][l + 4]);
+    } else {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[a][l] = 0.0;
+    }
+#pragma unroll
+    for (int i = n32; i < n1; i += 16)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          const double v = __dsub_rn(x[i + 4 * a + l], c[i + 4 * a + l]);
+          acc[a][l] = __fma_rn(v, v, acc[a][l]);
+        }
+    double s[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      s[l] = __dadd_rn(__dadd_rn(__dadd_rn(acc[0][l], acc[1][l]), acc[2][l]), acc[3][l]);
+    dot = __dadd_rn(__dadd_rn(s[0], s[2]), __dadd_rn(s[1], s[3]));
+  }
+#pragma unroll
+  for (int i = n1; i < DP; ++i) {
+    const double v = __dsub_rn(x[i], c[i]);
+    dot = __fma_rn(v, v, dot);
+  }
+  return dot;
+}
+
 template <int DP, typename XS, typename CS>
 __device__ __forceinline__ double exact_sq(const XS& x, const CS& c, int d) {
+  if (d == DP) return exact_sq_fixed<DP>(x, c);
   const int n1 = d & ~15, n32 = n1 & ~31;
   double dot = 0.0;
   if (n1) {
