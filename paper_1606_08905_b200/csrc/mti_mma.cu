@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   __syncwarp();
 
   // async gather of queued entries [base, base + cnum) into a staging tile (rows 0..cnum-1)
-  auto gather = [&](unsigned char* dst, int base, int cnum) {
+  auto gather = [&](unsigned char* dstp, int base, int cnum) {
+    const uint32_t dst = smem_u32(dstp);
     // source of each lane's row: HBM rows, the HBM row cache (semi-external runs), or
     // host memory
     const double* src = nullptr;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
       if (lane < cnum) {
 #pragma unroll
         for (int q2 = 0; q2 < DP / 2; ++q2)
-          if (2 * q2 < d) cp_async16(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
+          if (2 * q2 < d) cp_async16_s(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
       }
     } else {
       if (vec) {
@@ -145,12 +146,12 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
           const int r = (i < tot ? i : tot - 1) / hd, q2 = i - r * hd;
           const double* p = reinterpret_cast<const double*>(
               __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), r));
-          if (i < tot) cp_async16(dst + TL::chunk_off(r, q2, BR), p + 2 * q2);
+          if (i < tot) cp_async16_s(dst + TL::chunk_off(r, q2, BR), p + 2 * q2);
         }
       } else if (lane < cnum) {
 #pragma unroll
         for (int e = 0; e < DP; ++e)
-          if (e < d) cp_async8(dst + TL::elem_off(lane, e, BR), src + e);
+          if (e < d) cp_async8_s(dst + TL::elem_off(lane, e, BR), src + e);
       }
     }
     cp_async_commit();
@@ -186,7 +187,10 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   // filtered (and across calls), so the loads' latency overlaps useful work.
   long long blk = gw;
   constexpr int FB = DP <= 32 ? 4 : 2;  // (DP = 64 is register-bound)
-  constexpr bool PREFETCH = DP <= 16;    // wide rows: scoring dominates, keep the registers
+#ifndef KNB_MTI_PREFETCH_DP
+#define KNB_MTI_PREFETCH_DP 16
+#endif
+  constexpr bool PREFETCH = DP <= KNB_MTI_PREFETCH_DP;  // DP = 64: scoring dominates, keep the registers
   int pa[FB], ps[FB];
   double pu[FB];
   auto load_group = [&](long long b) {
