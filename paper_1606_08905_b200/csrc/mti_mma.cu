@@ -85,6 +85,9 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   int* qrow = reinterpret_cast<int*>(wbase + L.q_off);
   int* qorig = qrow + 192;
   int* qsrc = qrow + 384;  // semi-external runs: the row's HBM cache slot (-1: host memory)
+  // the queue is a ring of 192 entries starting at qh (popping a batch moves qh, no copies)
+  int qh = 0;
+  auto ring = [&](int i) { const int x = qh + i; return x >= 192 ? x - 192 : x; };
   double* acc = reinterpret_cast<double*>(wbase + L.acc_off);
   double* cnt = reinterpret_cast<double*>(wbase + L.cnt_off);
   double* sqa = reinterpret_cast<double*>(wbase + L.sq_off);
@@ -124,8 +127,9 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
     const double* src = nullptr;
     bool host = false;
     if (lane < cnum) {
-      const int r = qrow[base + lane];
-      const int slot = cslot ? qsrc[base + lane] : -1;
+      const int qi = ring(base + lane);
+      const int r = qrow[qi];
+      const int slot = cslot ? qsrc[qi] : -1;
       src = slot >= 0 ? a.cache + (long long)slot * d : a.X + (long long)r * d;
       host = a.row_gather && slot < 0;
     }
@@ -164,12 +168,12 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
     const bool valid = r < cnum;
     int id = sc.id;
     const double nd = exact_winner<DP>(tb, r, crow, k, d, sc.flag, id, nullptr);
-    const int orig = valid ? qorig[r] : 0;
+    const int orig = valid ? qorig[ring(r)] : 0;
     const bool moved = valid && id != orig;
     // ||x||^2 only for the (few) moved rows whose signed deltas carry it
     const double sq = moved ? row_self_sq<DP>(tb, r, d) : 0.0;
     if (valid) {
-      const long long grow = qrow[r];
+      const long long grow = qrow[ring(r)];
       a.upper[grow] = nd;
       a.tight[grow] = 1;
       if (moved) {
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
         }
         const unsigned b = __ballot_sync(0xffffffffu, live);
         if (live) {
-          const int pos = qn + __popc(b & ((1u << lane) - 1u));
+          const int pos = ring(qn + __popc(b & ((1u << lane) - 1u)));
           qrow[pos] = (int)row;
           qorig[pos] = aa[j];
           if (HOST && cslot) qsrc[pos] = sl[j];
@@ -269,21 +273,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
     process(tcur, b0);
     // pop the processed batch from the queue
     const int rest = qn - b0;
-    for (int i0 = 0; i0 < rest; i0 += 32) {
-      int rr = 0, ro = 0, rs = 0;
-      if (i0 + lane < rest) {
-        rr = qrow[b0 + i0 + lane];
-        ro = qorig[b0 + i0 + lane];
-        if (HOST && cslot) rs = qsrc[b0 + i0 + lane];
-      }
-      __syncwarp();
-      if (i0 + lane < rest) {
-        qrow[i0 + lane] = rr;
-        qorig[i0 + lane] = ro;
-        if (HOST && cslot) qsrc[i0 + lane] = rs;
-      }
-      __syncwarp();
-    }
+    qh = ring(b0);
     qn = rest;
     b0 = b1;
     cur ^= 1;
