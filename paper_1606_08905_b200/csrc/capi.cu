@@ -10,6 +10,9 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/knor_b200.h"
@@ -119,19 +122,67 @@ struct knb_ctx {
   long long t_host = 0;
   bool centroids_set = false;
   long long bytes = 0;
+  std::unordered_set<void*> pooled;  // allocations from the library's stream-ordered pool
 };
 
 namespace {
 
+// One stream-ordered memory pool per device for every context's buffers: a context's
+// create / destroy then costs no cudaMalloc / cudaFree (each an implicit device
+// synchronisation) once the pool holds the memory -- repeated kmeans() calls reuse it.
+// Up to 16 GiB stays reserved between contexts; beyond that the pool returns memory to
+// the driver at the next synchronisation.
+cudaMemPool_t lib_pool(int device) {
+  static std::mutex mu;
+  static std::unordered_map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(device);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    pool = nullptr;
+  } else {
+    uint64_t keep = 16ULL << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  pools[device] = pool;
+  return pool;
+}
+
 template <typename T>
 int dev_alloc(knb_ctx* c, T** p, size_t count) {
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  const size_t bytes = count * sizeof(T);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  cudaMemPool_t pool = cs == cudaStreamCaptureStatusNone ? lib_pool(c->device) : nullptr;
+  cudaError_t e;
+  if (pool) {
+    e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, c->stream);
+    if (e == cudaSuccess) {
+      c->pooled.insert(*p);
+      // usable from any stream and by synchronous copies from here on
+      e = cudaStreamSynchronize(c->stream);
+    }
+  } else {
+    e = cudaMalloc(reinterpret_cast<void**>(p), bytes);  // inside a capture: a plain allocation
+  }
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? KNB_E_NOMEM : KNB_E_CUDA,
-                std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + " B): " + cudaGetErrorString(e));
-  c->bytes += (long long)(count * sizeof(T));
+                std::string("device allocation (") + std::to_string(bytes) + " B): " + cudaGetErrorString(e));
+  c->bytes += (long long)bytes;
   return KNB_OK;
+}
+
+void dev_free(knb_ctx* c, void* p) {
+  if (!p) return;
+  if (c->pooled.erase(p)) cudaFreeAsync(p, c->stream);
+  else cudaFree(p);
 }
 
 FinalArgs final_args(knb_ctx* c) {
@@ -632,9 +683,9 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     knb_destroy(c);
     return code;
   };
-  cudaDeviceProp p;
-  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return bail(fail(KNB_E_CUDA, "cudaGetDeviceProperties"));
-  c->sms = p.multiProcessorCount;
+  // (one attribute query: cudaGetDeviceProperties costs milliseconds per call)
+  if (cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return bail(fail(KNB_E_CUDA, "cudaDeviceGetAttribute"));
   if (stream) {
     c->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -716,9 +767,9 @@ int knb_destroy(knb_ctx* c) {
                   c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records,
                   c->semA.fetched, c->semA.cslot, c->semA.crow, c->semA.cache, c->semA.bcount, c->semA.bpre,
                   c->semA.plo, c->semA.io};
-  for (void* q : ptrs)
-    if (q) cudaFree(q);
-  if (c->own_exch && c->exch) cudaFree(c->exch);
+  for (void* q : ptrs) dev_free(c, q);
+  if (c->own_exch && c->exch) dev_free(c, c->exch);
+  if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->host_registered) cudaHostUnregister(const_cast<void*>(c->host_registered));
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -863,7 +914,7 @@ int knb_set_exchange(knb_ctx* c, double* dev, int64_t len) {
   if (c->own_exch && c->exch) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    cudaFree(c->exch);
+    dev_free(c, c->exch);
     c->bytes -= (long long)(c->L * sizeof(double));
   }
   c->exch = dev;
@@ -893,7 +944,7 @@ int knb_init_gather(knb_ctx* c, const int64_t* ids, int32_t count) {
   if (rc) return rc;
   if (count < 1 || count > c->k || !ids) return fail(KNB_E_ARG, "gather count must be in [1, k]");
   if (count > c->ids_cap) {
-    if (c->ids_dev) cudaFree(c->ids_dev);
+    dev_free(c, c->ids_dev);
     c->ids_dev = nullptr;
     if ((rc = dev_alloc(c, &c->ids_dev, c->k))) return rc;
     c->ids_cap = c->k;
@@ -1027,10 +1078,10 @@ int knb_kpp_run(knb_ctx* c, int64_t first_pick, const double* u_host, int32_t k,
   double* scal = nullptr;
   if ((rc = dev_alloc(c, &picks, (size_t)k))) return rc;
   auto cleanup = [&]() {
-    cudaFree(picks);
-    if (u) cudaFree(u);
-    if (degen) cudaFree(degen);
-    if (scal) cudaFree(scal);
+    dev_free(c, picks);
+    dev_free(c, u);
+    dev_free(c, degen);
+    dev_free(c, scal);
     c->bytes -= (long long)(k * 8 + (k > 1 ? (k - 1) * 8 : 8) + 4 + 16);
   };
   if ((rc = dev_alloc(c, &u, (size_t)(k > 1 ? k - 1 : 1))) || (rc = dev_alloc(c, &degen, 1)) ||
@@ -1079,7 +1130,7 @@ int knb_kpp_release(knb_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->d2) {
-    cudaFree(c->d2);
+    dev_free(c, c->d2);
     c->bytes -= (long long)(sizeof(double) * (c->n_local ? c->n_local : 1));
   }
   c->d2 = nullptr;
