@@ -25,30 +25,39 @@ namespace knb {
 
 namespace {
 
-// 8 lanes per element: lane q sums CTA partials [q*S, (q+1)*S) in CTA order (S =
-// ceil(G/8), all loads in flight), then the 8 sums combine in a fixed butterfly.
+// LPE lanes per element: lane q sums CTA partials [q*S, (q+1)*S) in CTA order
+// (S = ceil(G/LPE), loads batched 16 deep), then the LPE sums combine in a fixed
+// butterfly -- a fixed order for a given (G, L), so runs are bit-reproducible.  Short
+// vectors (the usual case: k*d + 2k + 8 doubles) take 32 lanes per element so that
+// every partial's load is in flight at once; the pass is one memory round trip.
+template <int LPE>
 __global__ void reduce_kernel(const double* __restrict__ partials, int G, long long L,
                               double* __restrict__ out, const Ctrl* ctrl) {
   if (ctrl->stop && !ctrl->ignore_stop) return;
-  const int q = threadIdx.x & 7;
-  const int S = (G + 7) / 8;
+  constexpr int EPW = 32 / LPE;  // elements per warp
+  const int q = threadIdx.x & (LPE - 1);
+  const int S = (G + LPE - 1) / LPE;
   const int b0 = q * S, b1 = b0 + S < G ? b0 + S : G;
-  for (long long e0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3; e0 < ((L + 3) / 4) * 4;
-       e0 += ((long long)gridDim.x * blockDim.x) >> 3) {
+  for (long long e0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / LPE; e0 < ((L + EPW - 1) / EPW) * EPW;
+       e0 += ((long long)gridDim.x * blockDim.x) / LPE) {
     const long long e = e0 < L ? e0 : L - 1;
     double s = 0.0;
     int b = b0;
-    for (; b + 8 <= b1; b += 8) {
-      double v[8];
+    for (; b + 16 <= b1; b += 16) {
+      double v[16];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = partials[(long long)(b + t) * L + e];
+      for (int t = 0; t < 16; ++t) v[t] = partials[(long long)(b + t) * L + e];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) s += v[t];
+      for (int t = 0; t < 16; ++t) s += v[t];
     }
-    for (; b < b1; ++b) s += partials[(long long)b * L + e];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    double v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = b + t < b1 ? partials[(long long)(b + t) * L + e] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (b + t < b1) s += v[t];
+#pragma unroll
+    for (int o = 1; o < LPE; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (q == 0 && e0 < L) out[e] = s;
   }
 }
@@ -274,9 +283,14 @@ __global__ void cmax_kernel(const FinalArgs f) {
 
 cudaError_t launch_reduce(const double* partials, int G, long long L, double* out, const Ctrl* ctrl,
                           cudaStream_t s) {
-  long long blocks = (L * 8 + 127) / 128;  // 8 lanes per element, small blocks
-  if (blocks > 4096) blocks = 4096;
-  reduce_kernel<<<(int)blocks, 128, 0, s>>>(partials, G, L, out, ctrl);
+  if (L <= 8192) {  // latency-bound: every partial in flight
+    const long long blocks = (L * 32 + 127) / 128;
+    reduce_kernel<32><<<(int)blocks, 128, 0, s>>>(partials, G, L, out, ctrl);
+  } else {
+    long long blocks = (L * 8 + 127) / 128;
+    if (blocks > 4096) blocks = 4096;
+    reduce_kernel<8><<<(int)blocks, 128, 0, s>>>(partials, G, L, out, ctrl);
+  }
   return cudaGetLastError();
 }
 
