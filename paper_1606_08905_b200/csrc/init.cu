@@ -66,49 +66,96 @@ __global__ void kpp_update_kernel(const T* __restrict__ X, long long n, int d,
   }
 }
 
-// Same contract and summation order as kpp_update_kernel for f64 rows with d <= DP:
-// the row is loaded into registers with 16-byte loads and the centroid is read from
-// shared memory, so the pass runs at memory speed.
+// Same contract and summation order as kpp_update_kernel (thread i of a block handles
+// rows lo + i, lo + i + 256, ...) for f64 rows with d <= DP, at memory speed: 256-row
+// slabs stream into shared memory with coalesced 16-byte cp.async copies (consecutive
+// threads, consecutive bytes; the next slab in flight while this one is scored), and
+// every thread reads its row from there (row stride DP + 2 doubles: conflict-free
+// 16-byte reads).
+constexpr int KPP_SLAB = 256;
 template <int DP>
-__global__ void kpp_update_reg_kernel(const double* __restrict__ X, long long n, int d, const double* __restrict__ c,
-                                      double* __restrict__ d2, int first, double* __restrict__ block_sums) {
+__host__ __device__ constexpr size_t kpp_tile_bytes() { return 2ull * KPP_SLAB * (DP + 2) * 8; }
+
+template <int DP>
+__global__ void __launch_bounds__(KPP_SLAB) kpp_update_reg_kernel(const double* __restrict__ X, long long n, int d,
+                                                                 const double* __restrict__ c,
+                                                                 double* __restrict__ d2, int first,
+                                                                 double* __restrict__ block_sums) {
+  constexpr int RS = DP + 2;
   __shared__ double sh[32];
   __shared__ double cs[DP];
-  for (int e = threadIdx.x; e < DP; e += blockDim.x) cs[e] = e < d ? c[e] : 0.0;
-  __syncthreads();
-  const long long b = blockIdx.x;
-  const long long lo = b * KPP_BLOCK;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < KPP_BLOCK; i += blockDim.x) {
-    const long long r = lo + i;
-    if (r >= n) break;
-    double x[DP];
-    const double2* xr = reinterpret_cast<const double2*>(X + r * d);
-#pragma unroll
-    for (int q = 0; q < DP / 2; ++q) {
-      if (2 * q < d) {
-        const double2 v = xr[q];
-        x[2 * q] = v.x;
-        x[2 * q + 1] = v.y;
-      } else {
-        x[2 * q] = 0.0;
-        x[2 * q + 1] = 0.0;
-      }
+  extern __shared__ __align__(16) double tiles[];  // two slabs
+  const int tid = threadIdx.x;
+  for (int e = tid; e < DP; e += blockDim.x) cs[e] = e < d ? c[e] : 0.0;
+  const long long lo = (long long)blockIdx.x * KPP_BLOCK;
+  const int hd = d >> 1;
+  const int nslab = (int)((n - lo < KPP_BLOCK ? n - lo : KPP_BLOCK) + KPP_SLAB - 1) / KPP_SLAB;
+  const uint32_t t0 = smem_u32(tiles);
+  auto issue = [&](int j) {
+    const long long r0 = lo + (long long)j * KPP_SLAB;
+    const int rows = n - r0 < KPP_SLAB ? (int)(n - r0) : KPP_SLAB;
+    const double2* src = reinterpret_cast<const double2*>(X + r0 * d);
+    const uint32_t dst = t0 + (uint32_t)((j & 1) * KPP_SLAB * RS * 8);
+    for (int ch = tid; ch < rows * hd; ch += KPP_SLAB) {
+      const int r = ch / hd, q = ch - r * hd;
+      cp_async16_s(dst + (uint32_t)((r * RS + 2 * q) * 8), src + ch);
     }
-    const double dist = sqrt(exact_sq<DP>(x, cs, d));
-    const double cand = dist * dist;
-    double v = first ? cand : fmin(d2[r], cand);
-    d2[r] = v;
-    s += v;
+    cp_async_commit();
+  };
+  double s = 0.0;
+  if (nslab > 0) issue(0);
+  for (int j = 0; j < nslab; ++j) {
+    if (j + 1 < nslab) {
+      issue(j + 1);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    const long long r0 = lo + (long long)j * KPP_SLAB;
+    const int rows = n - r0 < KPP_SLAB ? (int)(n - r0) : KPP_SLAB;
+    if (tid < rows) {
+      const double old = first ? 0.0 : d2[r0 + tid];  // issued before the row's arithmetic
+      const double* row = tiles + (j & 1) * KPP_SLAB * RS + tid * RS;
+      double x[DP];
+#pragma unroll
+      for (int q = 0; q < DP / 2; ++q) {
+        if (2 * q < d) {
+          const double2 v = *reinterpret_cast<const double2*>(row + 2 * q);
+          x[2 * q] = v.x;
+          x[2 * q + 1] = v.y;
+        } else {
+          x[2 * q] = 0.0;
+          x[2 * q + 1] = 0.0;
+        }
+      }
+      const long long r = r0 + tid;
+      const double dist = sqrt(exact_sq<DP>(x, cs, d));
+      const double cand = dist * dist;
+      const double v = first ? cand : fmin(old, cand);
+      d2[r] = v;
+      s += v;
+    }
+    __syncthreads();  // slab j's buffer is refilled by issue(j + 2)
   }
   s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  if ((tid & 31) == 0) sh[tid >> 5] = s;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
-    block_sums[b] = t;
+    block_sums[blockIdx.x] = t;
   }
+}
+
+template <int DP>
+cudaError_t launch_kpp_tile(const double* X, long long n, int d, const double* c, double* d2, int first,
+                            double* block_sums, int nblk, cudaStream_t s) {
+  const size_t sm = kpp_tile_bytes<DP>();
+  cudaError_t e = cudaFuncSetAttribute(kpp_update_reg_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  kpp_update_reg_kernel<DP><<<nblk, KPP_SLAB, sm, s>>>(X, n, d, c, d2, first, block_sums);
+  return cudaGetLastError();
 }
 
 // block sums of p = d2 / total
@@ -196,52 +243,87 @@ __global__ void kpp_search_kernel(const double* __restrict__ d2, long long n, do
   kpp_search_body(d2, n, total, bs, nblk, thr, out);
 }
 
+// inclusive scan of one value per thread over the CTA (fixed shape: warp shuffles, then
+// the warp totals), plus the CTA total; blockDim.x == 1024
+__device__ __forceinline__ double cta_scan(double v, double* wsum, double* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) wsum[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double z = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  const double r = v + (w ? wsum[w - 1] : 0.0);
+  *total = wsum[31];
+  __syncthreads();
+  return r;
+}
+
+// The pick: the first row whose running sum of p = d2 / total exceeds thr, found in
+// two parallel scans (block sums, 1024 at a time with a carried base; then the 2048
+// rows of the crossing block, two per thread).  Fixed arithmetic order, so the pick
+// is deterministic; it differs from a sequential walk only by rounding.
 __device__ void kpp_search_body(const double* __restrict__ d2, long long n, double total,
                                 const double* __restrict__ bs, int nblk, double thr, long long* out) {
-  __shared__ double run_sh;
-  __shared__ int blk_sh;
-  __shared__ double part[1024];
-  if (threadIdx.x == 0) {
-    double run = 0.0;
-    int b = 0;
-    for (; b < nblk; ++b) {
-      if (run + bs[b] > thr) break;
-      run += bs[b];
+  __shared__ double wsum[32];
+  __shared__ double incl_sh[1024];
+  __shared__ int found_sh;
+  const int tid = threadIdx.x;
+  double base = 0.0;  // sum of the blocks before the current chunk
+  int blk = -1;
+  for (int c0 = 0; c0 < nblk; c0 += 1024) {
+    const int b = c0 + tid;
+    if (tid == 0) found_sh = 0x7fffffff;
+    double tot;
+    const double incl = base + cta_scan(b < nblk ? bs[b] : 0.0, wsum, &tot);
+    incl_sh[tid] = incl;
+    if (b < nblk && incl > thr) atomicMin(&found_sh, tid);
+    __syncthreads();
+    const int f = found_sh;
+    if (f != 0x7fffffff) {
+      blk = c0 + f;
+      base = f ? incl_sh[f - 1] : base;
+      break;
     }
-    if (b == nblk) b = nblk - 1;  // rounding at the very end: clamp like searchsorted's last bin
-    blk_sh = b;
-    // recompute the base as the sum of the preceding blocks (already in run)
-    run_sh = run;
+    base += tot;
+    __syncthreads();
+  }
+  if (blk < 0) {  // rounding at the very end: the last bin, like searchsorted
+    blk = nblk - 1;
+    base -= bs[nblk - 1];
   }
   __syncthreads();
-  const long long lo = (long long)blk_sh * KPP_BLOCK;
-  const int per = KPP_BLOCK / blockDim.x;  // rows per thread (contiguous)
-  double s = 0.0;
-  for (int i = 0; i < per; ++i) {
-    const long long r = lo + threadIdx.x * per + i;
-    if (r < n) s += d2[r] / total;
-  }
-  part[threadIdx.x] = s;
+  const long long lo = (long long)blk * KPP_BLOCK;
+  // two rows per thread, in order
+  const long long r0 = lo + 2LL * tid, r1 = r0 + 1;
+  const double p0 = r0 < n ? d2[r0] / total : 0.0;
+  const double p1 = r1 < n ? d2[r1] / total : 0.0;
+  if (tid == 0) found_sh = 0x7fffffff;
+  double tot;
+  const double incl = base + cta_scan(p0 + p1, wsum, &tot);
+  incl_sh[tid] = incl;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double run = run_sh;
-    long long found = -1;
-    for (int t = 0; t < (int)blockDim.x && found < 0; ++t) {
-      if (run + part[t] > thr) {
-        for (int i = 0; i < per; ++i) {
-          const long long r = lo + (long long)t * per + i;
-          if (r >= n) break;
-          run += d2[r] / total;
-          if (run > thr) { found = r; break; }
-        }
-        if (found < 0) found = lo + (long long)t * per + per - 1;
-      } else {
-        run += part[t];
-      }
-    }
-    if (found < 0) found = n - 1;
-    if (found >= n) found = n - 1;
-    *out = found;
+  const double before = tid ? incl_sh[tid - 1] : base;
+  if (r0 < n) {
+    if (before + p0 > thr) atomicMin(&found_sh, 2 * tid);
+    else if (r1 < n && incl > thr) atomicMin(&found_sh, 2 * tid + 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long f = found_sh == 0x7fffffff ? lo + KPP_BLOCK - 1 : lo + found_sh;  // (rounding: the block's end)
+    if (f >= n) f = n - 1;
+    *out = f;
   }
 }
 
@@ -293,11 +375,11 @@ cudaError_t launch_kpp_update(const void* X, int elem, long long n, int d, const
   const bool vec = elem == 8 && (d % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
   const double* Xd = static_cast<const double*>(X);
   if (vec && d <= 8)
-    kpp_update_reg_kernel<8><<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
+    return launch_kpp_tile<8>(Xd, n, d, c, d2, first, block_sums, nblk, s);
   else if (vec && d <= 16)
-    kpp_update_reg_kernel<16><<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
+    return launch_kpp_tile<16>(Xd, n, d, c, d2, first, block_sums, nblk, s);
   else if (vec && d <= 32)
-    kpp_update_reg_kernel<32><<<nblk, 256, 0, s>>>(Xd, n, d, c, d2, first, block_sums);
+    return launch_kpp_tile<32>(Xd, n, d, c, d2, first, block_sums, nblk, s);
   else if (elem == 4)
     kpp_update_kernel<<<nblk, 256, 0, s>>>(static_cast<const float*>(X), n, d, c, d2, first, block_sums);
   else
@@ -318,7 +400,7 @@ cudaError_t launch_sum_blocks(const double* block_sums, int nblk, double* out, c
 
 cudaError_t launch_kpp_search(const double* d2, long long n, double total, const double* block_sums, int nblk,
                               double threshold, long long* out, cudaStream_t s) {
-  kpp_search_kernel<<<1, 256, 0, s>>>(d2, n, total, block_sums, nblk, threshold, out);
+  kpp_search_kernel<<<1, 1024, 0, s>>>(d2, n, total, block_sums, nblk, threshold, out);
   return cudaGetLastError();
 }
 
@@ -331,7 +413,7 @@ cudaError_t launch_kpp_psums_dev(const double* d2, long long n, const double* to
 cudaError_t launch_kpp_search_dev(const double* d2, long long n, const double* total, const double* block_sums,
                                   int nblk, const double* cdf_end, const double* u, long long* out, int* degenerate,
                                   cudaStream_t s) {
-  kpp_search_dev_kernel<<<1, 256, 0, s>>>(d2, n, total, block_sums, nblk, cdf_end, u, out, degenerate);
+  kpp_search_dev_kernel<<<1, 1024, 0, s>>>(d2, n, total, block_sums, nblk, cdf_end, u, out, degenerate);
   return cudaGetLastError();
 }
 

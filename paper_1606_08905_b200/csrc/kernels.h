@@ -213,6 +213,6 @@ cudaError_t launch_validate(const double* X, long long n, int d, int k, const in
 cudaError_t launch_check_finite(const void* X, int elem, long long n, int d, long long* first_bad,
                                 cudaStream_t s);
 
-constexpr int KPP_BLOCK = 4096;  // rows per kmeans++ probability block
+constexpr int KPP_BLOCK = 2048;  // rows per kmeans++ probability block (about 7 waves of CTAs at c2)
 
 }  // namespace knb
