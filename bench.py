@@ -24,6 +24,7 @@ host with all cores, on a bounded row sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -53,20 +54,45 @@ def load_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler (start before the timed region, stop after)."""
+    """nvidia-smi sampler (every 100 ms, from before the warm-up to after the timed loops).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    ``mark_start`` / ``mark_stop`` bracket the timed region; the report uses the samples
+    taken inside it, or -- when the region is shorter than the sampling period -- the
+    nearest sample on each side (the GPU is busy with warm-up and the local-pass loop
+    there), and says which in ``"window"``."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.t0 = self.t1 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+
+    def wait_first(self, timeout: float = 3.0) -> None:
+        """Block until the sampler has written its first line (nvidia-smi starts slowly)."""
+        end = time.time() + timeout
+        while self.p is not None and time.time() < end and os.path.getsize(self.f.name) == 0:
+            time.sleep(0.02)
+
+    def mark_start(self) -> None:
+        self.t0 = time.time()
+
+    def mark_stop(self) -> None:
+        self.t1 = time.time()
+
+    @staticmethod
+    def _ts(field: str):
+        try:
+            return datetime.datetime.strptime(field.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
 
     def stop(self) -> dict:
         if self.p is None:
@@ -76,21 +102,33 @@ class Clocks:
         self.f.seek(0)
         rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
         os.unlink(self.f.name)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        samples = []
         for r in rows:
+            ts = self._ts(r[0])
             try:
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
+                samples.append((ts, float(r[1]), float(r[2]), r))
             except ValueError:
                 continue
-            for nm, v in zip(names, r[5:9]):
+        window = "timed region"
+        t0, t1 = self.t0, self.t1
+        inside = [x for x in samples if t0 is None or (x[0] is not None and t0 <= x[0] <= t1)]
+        if not inside and samples:
+            before = [x for x in samples if x[0] is not None and x[0] < t0]
+            after = [x for x in samples if x[0] is not None and x[0] > t1]
+            inside = before[-1:] + after[:1]
+            window = f"nearest samples around a {1e3 * (t1 - t0):.1f} ms timed region"
+        sm = [x[1] for x in inside]
+        mx = [x[2] for x in inside]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for x in inside:
+            for nm, v in zip(names, x[3][5:9]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
-        load = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        load = [v for v in sm if mx and v > 0.5 * max(mx)] or sm
         return {"sm_mhz": statistics.median(load) if load else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def workload(name: str, n: int | None):
@@ -190,6 +228,7 @@ def run_ours(args):
     elem = dev_rows.element_size()
     shard_bytes = (hi - lo) * d * elem
 
+    clocks = Clocks(local_rank)  # started early: its first sample precedes the timed region
     peaks = load_peaks()
     mp = _native.measure_peaks(local_rank)
     hbm_peak = peaks.get("hbm_gbs") or 6650.0
@@ -197,7 +236,6 @@ def run_ours(args):
     # kind::tf32 runs at half the bf16 rate on sm_100: half the measured cuBLAS bf16 figure
     tf32_peak = 0.5 * (peaks.get("bf16_tflops") or 2250.0) * 1e12
 
-    clocks = Clocks(local_rank)
     total_iters = args.warmup + 2 * args.steps + 2
     ecfg = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"], max_iters=total_iters,
                            tolerance=cfg["tolerance"], device=local_rank, mti_scan=args.mti_scan)
@@ -239,6 +277,8 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
     torch.cuda.synchronize()
+    clocks.wait_first()
+    clocks.mark_start()
     start.record(stream)
     if world == 1 and not force_comm:
         run.ctx.enqueue(args.steps)  # one CUDA graph replay per iteration
@@ -252,6 +292,7 @@ def run_ours(args):
             run.finish()
     stop.record(stream)
     torch.cuda.synchronize()
+    clocks.mark_stop()
     if world > 1:
         torch.distributed.barrier()
     ms = start.elapsed_time(stop)
