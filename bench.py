@@ -53,6 +53,19 @@ def load_peaks():
         return {}
 
 
+def measured_traffic(config: str):
+    """DRAM bytes (read + write) per launch of the config's dominant kernel from the
+    committed ncu capture (profiles/r01_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as fh:
+            t = json.load(fh).get(config)
+    except (OSError, ValueError):
+        return None, None
+    if not t:
+        return None, None
+    return t["traffic_bytes"], f"{t['kernel']}: {t['source']}"
+
+
 class Clocks:
     """nvidia-smi sampler (every 100 ms, from before the warm-up to after the timed loops).
 
@@ -334,9 +347,10 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": bytes_ / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"], roof["traffic_source"] = measured_traffic(args.config)
     roof["kernel"] = ("tc_assign_kernel + tc_rerank + segsum" if tc else
-                      "mti_tile_kernel + reduce" if cfg["pruning"] else "dense_tile_kernel + reduce")
+                      "mti_mma_kernel (compacted survivors) + reduce" if cfg["pruning"] else
+                      "dense_mma_kernel + reduce")
     roof["kernel_ms"] = kern_s * 1e3
     roof["work"] = "dense-equivalent 2*n*k*d flops and n*d*8 point bytes per launch; MTI skips are not discounted"
     roof["computed_fraction"] = comps / max(1, n * k * len(timed_stats))
