@@ -191,10 +191,8 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
   // filtered (and across calls), so the loads' latency overlaps useful work.
   long long blk = gw;
   constexpr int FB = DP <= 32 ? 4 : 2;  // (DP = 64 is register-bound)
-#ifndef KNB_MTI_PREFETCH_DP
-#define KNB_MTI_PREFETCH_DP 16
-#endif
-  constexpr bool PREFETCH = DP <= KNB_MTI_PREFETCH_DP;  // DP = 64: scoring dominates, keep the registers
+  // (measured: prefetching at DP = 32 costs 1.6% at c2 -- the registers matter more)
+  constexpr bool PREFETCH = DP <= 16;
   int pa[FB], ps[FB];
   double pu[FB];
   auto load_group = [&](long long b) {
