@@ -98,3 +98,39 @@ def test_sem_equals_in_memory_any_capacity(tmp_path):
             post = [s for s in sem.iterations if s.t > 2]
             hits = sum(s.io.cache_hits for s in post)
             assert post and hits >= 0.9 * sum(s.io.cache_hits + s.io.cache_misses for s in post)
+
+
+def _oracle_io(m, k, seed, T, task_size, page, enabled, cap, start, pruning=True, max_iters=30, init="forgy"):
+    o = O.lloyd(m, k, init=init, seed=seed, pruning=pruning, max_iters=max_iters, T=T, task_size=task_size,
+                collect=True, collect_fetch=True)
+    cnt = OC.io_counters(o.fetched, [s.skips for s in o.iterations], *m.shape, T, task_size, page, enabled, cap,
+                         start)
+    return o, cnt
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=7, d=3, k=3, T=4, task_size=1, page=1, cap=48, start=1),          # tiny: empty-ish partitions, 1-byte pages
+    dict(n=3000, d=5, k=6, T=3, task_size=77, page=100, cap=3000 * 40 // 3, start=2),  # odd d (scalar gathers)
+    dict(n=2500, d=3, k=80, T=2, task_size=500, page=4096, cap=10**6, start=1),  # k > 64: generic MTI path
+    dict(n=4000, d=33, k=9, T=5, task_size=129, page=4096, cap=4000 * 264 // 5, start=3),  # DP = 64 rows
+    dict(n=5000, d=8, k=7, T=2, task_size=8192, page=4096, cap=8 * 64 - 1, start=1),  # capacity below 2 rows / partition
+])
+def test_sem_edge_cases_against_oracle(tmp_path, case):
+    m = kb.synth.mixture(kb.synth.MixtureSpec(case["n"], case["d"], min(case["k"], 8), 5, "uniform", -3, 3, 1.0))
+    path = tmp_path / "e.raw"
+    m.tofile(path)
+    o, want = _oracle_io(m, case["k"], 3, case["T"], case["task_size"], case["page"], True, case["cap"],
+                         case["start"])
+    cfg = kb.EngineConfig(k=case["k"], seed=3, T=case["T"], task_size=case["task_size"], max_iters=30, mode="sem",
+                          collect_assignments=True)
+    with RowStore(path, case["n"], case["d"], page_size=case["page"]) as store:
+        res = kmeans_ondisk(store, cfg, cache_capacity=case["cap"], schedule=CacheSchedule(case["start"]),
+                            inspect_cache=True)
+    assert res.n_iterations == o.n_iterations
+    for a, b in zip(res.assignment_history, o.history):
+        assert np.array_equal(a, b)
+    assert np.array_equal(_io(res), want)
+    ids, rows = res.row_cache
+    want_ids = OC.cached_ids(o.fetched, case["n"], case["d"], case["T"], case["cap"], case["start"])
+    assert np.array_equal(np.sort(ids), np.sort(want_ids))
+    assert rows.tobytes() == m[ids].tobytes()
