@@ -214,6 +214,17 @@ int knb_describe(knb_ctx* ctx, int32_t* dense_dp, int32_t* use_tma, int32_t* gri
 int knb_fill_uniform_pcg64(double* dev_out, int64_t count, int64_t first_draw, uint64_t state_hi,
                            uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, void* stream);
 
+/* The reference's distance primitives on the device (context-free, host pointers, same
+ * exact recipe as the engine): block_distances / nearest_centroid (distance.py:42-82) --
+ * dist_out (m x k) and/or ids_out / best_out (ascending strict-less argmin per row); any
+ * output may be NULL.  knb_rowwise: rowwise_distances (distance.py:36-39, refs m x d or one
+ * shared row) or, with refs NULL, row_sqnorms (distance.py:66-72); take_sqrt selects the
+ * distance or the squared sum. */
+int knb_block_distances(int device, const double* rows, int64_t m, const double* cents, int32_t k, int32_t d,
+                        double* dist_out, int32_t* ids_out, double* best_out);
+int knb_rowwise(int device, const double* rows, int64_t m, const double* refs, int32_t shared_ref, int32_t d,
+                int32_t take_sqrt, double* out);
+
 /* Roofline denominators measured on the device: FP64 FMA rate (DFMA/s, 8 independent chains
  * per thread over 8 CTAs/SM) and a 1 GiB device copy (read + write bytes/s). */
 int knb_measure_peaks(int device, double* dfma_per_s, double* copy_bytes_per_s);

@@ -25,12 +25,30 @@ from .fileio import HEADER_SIZE, MatrixIOError, load_matrix, save_matrix
 from .matrix import MatrixFormatError, RowRange, check_matrix, partition_rows
 from .outofcore import CacheSchedule, RowStore, kmeans_ondisk, should_refresh
 from .parallel import LocalComm, TorchComm, shard_of
+from .primitives import (
+    CentroidGeometry,
+    block_distances,
+    centroid_geometry,
+    euclidean_distance,
+    init_centroids,
+    nearest_centroid,
+    row_sqnorms,
+    rowwise_distances,
+)
 from .report import deterministic_view, format_report, parse_report
 
 __version__ = "0.1.0"
 
 __all__ = [
     "CacheSchedule",
+    "CentroidGeometry",
+    "block_distances",
+    "centroid_geometry",
+    "euclidean_distance",
+    "init_centroids",
+    "nearest_centroid",
+    "row_sqnorms",
+    "rowwise_distances",
     "CentroidSet",
     "RowStore",
     "kmeans_ondisk",

@@ -94,6 +94,8 @@ SIGNATURES = {
     "knb_state_bytes": [_P, _PI64],
     "knb_describe": [_P, _PI32, _PI32, _PI32, _PI32],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
+    "knb_block_distances": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _P, _P, _P],
+    "knb_rowwise": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _I32, _P],
     "knb_set_option": [_P, _I32, _I64],
     "knb_fill_uniform_pcg64": [_P, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P],
 }

@@ -46,6 +46,11 @@ constexpr double KNB_TF32_ERR = 0x1.4p-9;
 
 }  // namespace
 
+// error reporting shared with the context-free entry points (primitives.cu)
+namespace knb {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace knb
+
 struct knb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
