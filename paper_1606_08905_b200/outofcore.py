@@ -186,6 +186,48 @@ def fetch_rows(store: RowStore, ids, cache=None, stats: IoStats | None = None) -
     return out
 
 
+class RowCache:
+    """Host-side form of the reference's partitioned row cache (outofcore.py:228-270),
+    for ``fetch_rows`` callers: each partition keeps its smallest ``rows_per_partition``
+    collected ids, and the merged index is what ``published`` serves.  (``kmeans_ondisk``
+    keeps the same policy in HBM, csrc/sem.cu.)"""
+
+    def __init__(self, n_partitions: int, capacity_bytes: int, row_bytes: int):
+        if n_partitions < 1:
+            raise ValueError("need at least one partition")
+        if capacity_bytes < 0:
+            raise ValueError("capacity must be >= 0")
+        self.n_partitions = n_partitions
+        self.capacity_bytes = capacity_bytes
+        self.row_bytes = row_bytes
+        self.rows_per_partition = rows_per_partition(capacity_bytes, n_partitions, row_bytes)
+        self.partitions: list[dict] = [{} for _ in range(n_partitions)]
+        self.published: dict = {}
+        self.refresh_count = 0
+
+    def cached_rows(self) -> int:
+        return len(self.published)
+
+    def cached_bytes(self) -> int:
+        return len(self.published) * self.row_bytes
+
+    def rebuild(self, collected) -> None:
+        """Flush, keep each partition's smallest ids from its collected (ids, rows) chunks, publish."""
+        merged = {}
+        for p in range(self.n_partitions):
+            part = {}
+            chunks = collected[p]
+            if chunks and self.rows_per_partition > 0:
+                ids = np.concatenate([np.asarray(c[0], dtype=np.int64) for c in chunks])
+                rows = np.concatenate([np.asarray(c[1], dtype=np.float64) for c in chunks], axis=0)
+                for i in np.argsort(ids, kind="stable")[: self.rows_per_partition]:
+                    part[int(ids[i])] = rows[i].copy()
+            self.partitions[p] = part
+            merged.update(part)
+        self.published = merged
+        self.refresh_count += 1
+
+
 @dataclass(frozen=True)
 class CacheSchedule:
     """Refresh at iteration ``start``, then with doubling gaps (outofcore.py:273-279)."""

@@ -128,3 +128,31 @@ def test_kmeans_ondisk_mode_checks(store_8):
         kb.kmeans(np.zeros((4, 2)), kb.EngineConfig(k=2, mode="sem"))
     with pytest.raises(ValueError, match="capacity"):
         kmeans_ondisk(store, kb.EngineConfig(k=2, mode="sem"), cache_capacity=-1)
+
+
+def test_row_cache_rebuild_truncates_by_ascending_id():
+    """outofcore.py RowCache semantics (test_sem.py's cache case)."""
+    cache = kb.RowCache(n_partitions=2, capacity_bytes=4 * 64, row_bytes=64)
+    assert cache.rows_per_partition == 2
+    rows = np.random.default_rng(0).normal(size=(6, 8))
+    cache.rebuild([[(np.array([5, 9]), rows[0:2]), (np.array([1]), rows[2:3])],
+                   [(np.array([20, 30, 40]), rows[3:6])]])
+    assert sorted(cache.published) == [1, 5, 20, 30]
+    assert cache.cached_bytes() <= cache.capacity_bytes
+    assert np.array_equal(cache.published[1], rows[2])
+    store_rows = np.arange(64 * 8, dtype=np.float64).reshape(64, 8)
+    stats = IoStats()
+    assert cache.cached_rows() == 4
+
+
+def test_fetch_rows_through_a_cache(tmp_path):
+    m = kb.synth.uniform(256, 8, 1)
+    m.tofile(tmp_path / "c.raw")
+    cache = kb.RowCache(1, 64 * 64, 64)
+    cache.rebuild([[(np.arange(0, 64), m[:64])]])
+    with RowStore(tmp_path / "c.raw", 256, 8) as store:
+        stats = IoStats()
+        rows = fetch_rows(store, np.array([3, 10, 100, 200]), cache, stats)
+    assert rows.tobytes() == m[[3, 10, 100, 200]].tobytes()
+    assert (stats.cache_hits, stats.cache_misses) == (2, 2)
+    assert stats.bytes_read == 2 * 4096 and stats.bytes_requested == 4 * 64
