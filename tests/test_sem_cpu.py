@@ -140,8 +140,6 @@ def test_row_cache_rebuild_truncates_by_ascending_id():
     assert sorted(cache.published) == [1, 5, 20, 30]
     assert cache.cached_bytes() <= cache.capacity_bytes
     assert np.array_equal(cache.published[1], rows[2])
-    store_rows = np.arange(64 * 8, dtype=np.float64).reshape(64, 8)
-    stats = IoStats()
     assert cache.cached_rows() == 4
 
 
