@@ -712,6 +712,9 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     const long long rows = dense_rows_per_tile(c->DP);
     const long long tiles = (nl + rows - 1) / rows;
     long long g = c->DP ? dense_tile_grid(c->DP, k, d, c->sms) : 4LL * c->sms;
+    // small shards: one CTA per SM (a second CTA per SM only adds setup and partials;
+    // measured c1, 200k rows: 0.029 -> 0.027 ms / iteration)
+    if (c->DP && nl < 4096LL * c->sms) g = c->sms;
     c->G_dense = (int)(tiles < g ? tiles : g);
   }
   {
