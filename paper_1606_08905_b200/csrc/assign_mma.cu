@@ -108,8 +108,14 @@ __device__ __forceinline__ void load_block(const CUtensorMap* tmap, uint64_t* ba
   }
 }
 
-template <int DP>
-__global__ void __launch_bounds__(KNB_NT, 1)
+#ifndef KNB_DENSE_2CTA_DP
+#define KNB_DENSE_2CTA_DP 8
+#endif
+
+// SMALLK (k <= 16): the scorer's one-step form; with narrow rows it leaves room for
+// two CTAs per SM (<= 128 registers, no spills)
+template <int DP, bool SMALLK>
+__global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 2 : 1)
     dense_mma_kernel(const __grid_constant__ CUtensorMap tmap, const DenseArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;         // k-steps of 4 dims
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(KNB_NT, 1)
       skips += (valid && !live) ? 1 : 0;
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
       if (lmask) {
-        const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+        const Scored sc = score_block<DP, SMALLK>(tb, bf, chn, ntile8, tolk, cmax2, lane);
         int nid = sc.id;
         const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr);
         const double sq = (live && nid != aa) ? row_self_sq<DP>(tb, my_r, d) : 0.0;
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(KNB_NT, 1)
         accumulate_in_row_order<DP>(row_mask(live && nid != aa, my_r), nid, aa, sq, tb, acc, cnt, sqa, d, lane);
       }
     } else if (!labels) {
-      const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+      const Scored sc = score_block<DP, SMALLK>(tb, bf, chn, ntile8, tolk, cmax2, lane);
       id = sc.id;
       double nd2;
       if (sc.flag || a.mti_seed) {
@@ -349,15 +355,21 @@ int warps_for(int DP, int k, int d) {
   return 0;
 }
 
-template <int DP>
-cudaError_t launch_mma_dp(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
+template <int DP, bool SMALLK>
+cudaError_t launch_mma_k(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
   const int W = warps_for(DP, a.k, a.d);
   if (!W) return cudaErrorInvalidValue;
   const WarpSmem L(DP, a.k, a.d, W);
-  cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e =
+      cudaFuncSetAttribute(dense_mma_kernel<DP, SMALLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  dense_mma_kernel<DP><<<grid, W * 32, L.total, s>>>(*tmap, a);
+  dense_mma_kernel<DP, SMALLK><<<grid, W * 32, L.total, s>>>(*tmap, a);
   return cudaGetLastError();
+}
+
+template <int DP>
+cudaError_t launch_mma_dp(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
+  return a.k <= 16 ? launch_mma_k<DP, true>(tmap, a, grid, s) : launch_mma_k<DP, false>(tmap, a, grid, s);
 }
 
 }  // namespace

@@ -97,7 +97,9 @@ struct Scored {
 // Score the 32 rows of a block (TileLayout<DP>, BR rows at tb) against every centroid.
 // bf: centroids in B-fragment order, chn: -||c||^2/2 (dummy columns -inf).
 // Each lane returns the result for its row owner_lane^-1(lane) = t4*8 + g.
-template <int DP>
+// SMALLK: at most two 8-centroid tiles (k <= 16) -- one step, no software pipeline, so
+// the second set of accumulators never needs registers
+template <int DP, bool SMALLK = false>
 __device__ __forceinline__ Scored score_block(const unsigned char* tb, const double* bf, const double* chn,
                                               int ntile8, double tolk, double cmax2, int lane) {
   using TL = TileLayout<DP>;
@@ -179,17 +181,22 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
       merge_later(best[pg], bid[pg], flag[pg], pb, pi, pf, tolhi[pg]);
     }
   };
-  double ca0[4][2], ca1[4][2], cb0[4][2], cb1[4][2];
+  double ca0[4][2], ca1[4][2];
   mma_step(0, ca0, ca1);
-  int q = 0;
+  if constexpr (SMALLK) {
+    epilogue(0, ca0, ca1);
+  } else {
+    double cb0[4][2], cb1[4][2];
+    int q = 0;
 #pragma unroll 1
-  for (; q + 2 < ntile8; q += 4) {
-    mma_step(q + 2, cb0, cb1);
-    epilogue(q, ca0, ca1);
-    if (q + 4 < ntile8) mma_step(q + 4, ca0, ca1);
-    epilogue(q + 2, cb0, cb1);
+    for (; q + 2 < ntile8; q += 4) {
+      mma_step(q + 2, cb0, cb1);
+      epilogue(q, ca0, ca1);
+      if (q + 4 < ntile8) mma_step(q + 4, ca0, ca1);
+      epilogue(q + 2, cb0, cb1);
+    }
+    if (q < ntile8) epilogue(q, ca0, ca1);
   }
-  if (q < ntile8) epilogue(q, ca0, ca1);
 #pragma unroll
   for (int pg = 0; pg < 4; ++pg) {
     combine(best[pg], bid[pg], flag[pg], tolhi[pg], 1);

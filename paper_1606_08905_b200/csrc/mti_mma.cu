@@ -59,10 +59,14 @@ struct MtiMmaSmem {
   }
 };
 
+#ifndef KNB_MTI_2CTA_DP
+#define KNB_MTI_2CTA_DP 8
+#endif
+
 // HOST: rows in host memory (row_gather) and/or the semi-external HBM row cache; the
 // HBM-resident instantiation keeps the plain per-lane gather
-template <int DP, bool HOST>
-__global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
+template <int DP, bool HOST, bool SMALLK>
+__global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1) mti_mma_kernel(const MtiArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(KNB_NT, 1) mti_mma_kernel(const MtiArgs a) {
 
   // score and update the first `cnum` queued survivors (cnum <= 32), staged in tb
   auto process = [&](const unsigned char* tb, int cnum) {
-    const Scored sc = score_block<DP>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+    const Scored sc = score_block<DP, SMALLK>(tb, bf, chn, ntile8, tolk, cmax2, lane);
     const int r = t4 * 8 + g;
     const bool valid = r < cnum;
     int id = sc.id;
@@ -313,22 +317,23 @@ int mti_warps_for(int DP, int k, int d, bool src = false) {
   return 0;
 }
 
-template <int DP, bool HOST>
+template <int DP, bool HOST, bool SMALLK>
 cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
   const bool src = HOST && a.cslot != nullptr;
   const int W = mti_warps_for(DP, a.k, a.d, src);
   if (!W) return cudaErrorInvalidValue;
   const MtiMmaSmem L(DP, a.k, a.d, W, src);
   cudaError_t e =
-      cudaFuncSetAttribute(mti_mma_kernel<DP, HOST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      cudaFuncSetAttribute(mti_mma_kernel<DP, HOST, SMALLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  mti_mma_kernel<DP, HOST><<<grid, W * 32, L.total, s>>>(a);
+  mti_mma_kernel<DP, HOST, SMALLK><<<grid, W * 32, L.total, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int DP>
 cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
-  return (a.row_gather || a.cslot) ? launch_host<DP, true>(a, grid, s) : launch_host<DP, false>(a, grid, s);
+  if (a.row_gather || a.cslot) return launch_host<DP, true, false>(a, grid, s);
+  return a.k <= 16 ? launch_host<DP, false, true>(a, grid, s) : launch_host<DP, false, false>(a, grid, s);
 }
 
 }  // namespace
