@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
   constexpr int KS = DP / 4;         // k-steps of 4 dims
   constexpr int NS = DP <= 8 ? 4 : 2;
   extern __shared__ __align__(1024) unsigned char smem[];
+  pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
   if (a.gate && a.ctrl->mti_choice != 1) return;  // the compacted MTI kernel runs this iteration
 
@@ -363,8 +364,7 @@ cudaError_t launch_mma_k(const CUtensorMap* tmap, const DenseArgs& a, int grid, 
   cudaError_t e =
       cudaFuncSetAttribute(dense_mma_kernel<DP, SMALLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  dense_mma_kernel<DP, SMALLK><<<grid, W * 32, L.total, s>>>(*tmap, a);
-  return cudaGetLastError();
+  return launch_pdl(dense_mma_kernel<DP, SMALLK>, dim3(grid), dim3(W * 32), L.total, s, *tmap, a);
 }
 
 template <int DP>

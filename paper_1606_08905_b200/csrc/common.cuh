@@ -372,6 +372,21 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// Programmatic dependent launch: the iteration's kernels are launched with
+// programmatic stream serialization, each lets its dependents launch as soon as it
+// starts and waits (griddepcontrol.wait: full completion and visibility of the
+// previous kernel) before touching any state, so launch latency overlaps the previous
+// kernel's tail.  Both are no-ops for a kernel launched without the attribute.
+#ifndef KNB_PDL
+#define KNB_PDL 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if KNB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // shared-window address forms (no generic -> shared conversion per copy)
 __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");

@@ -7,7 +7,28 @@
 
 #include "state.cuh"
 
+#ifndef KNB_PDL_LAUNCH
+#define KNB_PDL_LAUNCH 1
+#endif
+
 namespace knb {
+
+// launch with programmatic stream serialization (see pdl_enter in common.cuh)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = KNB_PDL_LAUNCH;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 struct DenseArgs {
   const double* X;       // n x d row-major (shard-local rows)

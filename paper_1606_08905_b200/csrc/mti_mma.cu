@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;
   extern __shared__ __align__(1024) unsigned char smem[];
+  pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
   if (a.gate && a.ctrl->mti_choice != 0) return;  // the block-dense pass runs this iteration
   const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -326,8 +327,7 @@ cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
   cudaError_t e =
       cudaFuncSetAttribute(mti_mma_kernel<DP, HOST, SMALLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  mti_mma_kernel<DP, HOST, SMALLK><<<grid, W * 32, L.total, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(mti_mma_kernel<DP, HOST, SMALLK>, dim3(grid), dim3(W * 32), L.total, s, a);
 }
 
 template <int DP>

@@ -33,6 +33,7 @@ namespace {
 template <int LPE>
 __global__ void reduce_kernel(const double* __restrict__ partials, int G, long long L,
                               double* __restrict__ out, const Ctrl* ctrl) {
+  pdl_enter();
   if (ctrl->stop && !ctrl->ignore_stop) return;
   constexpr int EPW = 32 / LPE;  // elements per warp
   const int q = threadIdx.x & (LPE - 1);
@@ -69,6 +70,7 @@ __device__ void geometry_row(const FinalArgs& f, int a);
 // One warp per centroid; the last CTA to finish then runs the statistics row (one
 // launch instead of two; the MTI geometry stays a separate, wider kernel).
 __global__ void finalize_kernel(const FinalArgs f) {
+  pdl_enter();
   if (f.ctrl->stop && !f.ctrl->ignore_stop) return;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j < f.k) finalize_centroid(f, j);
@@ -219,6 +221,7 @@ __device__ void geometry_row(const FinalArgs& f, int a) {
 }
 
 __global__ void geometry_kernel(const FinalArgs f) {
+  pdl_enter();
   const Ctrl* c = f.ctrl;
   if (c->stop && !c->ignore_stop) return;
   const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -285,25 +288,22 @@ cudaError_t launch_reduce(const double* partials, int G, long long L, double* ou
                           cudaStream_t s) {
   if (L <= 8192) {  // latency-bound: every partial in flight
     const long long blocks = (L * 32 + 127) / 128;
-    reduce_kernel<32><<<(int)blocks, 128, 0, s>>>(partials, G, L, out, ctrl);
+    return launch_pdl(reduce_kernel<32>, dim3((unsigned)blocks), dim3(128), 0, s, partials, G, L, out, ctrl);
   } else {
     long long blocks = (L * 8 + 127) / 128;
     if (blocks > 4096) blocks = 4096;
-    reduce_kernel<8><<<(int)blocks, 128, 0, s>>>(partials, G, L, out, ctrl);
+    return launch_pdl(reduce_kernel<8>, dim3((unsigned)blocks), dim3(128), 0, s, partials, G, L, out, ctrl);
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t s) {
   const int wpb = 8;
-  finalize_kernel<<<(f.k + wpb - 1) / wpb, wpb * 32, 0, s>>>(f);
-  return cudaGetLastError();
+  return launch_pdl(finalize_kernel, dim3((f.k + wpb - 1) / wpb), dim3(wpb * 32), 0, s, f);
 }
 
 cudaError_t launch_geometry(const FinalArgs& f, cudaStream_t s) {
   const int wpb = 8;
-  geometry_kernel<<<(f.k + wpb - 1) / wpb, wpb * 32, 0, s>>>(f);
-  return cudaGetLastError();
+  return launch_pdl(geometry_kernel, dim3((f.k + wpb - 1) / wpb), dim3(wpb * 32), 0, s, f);
 }
 
 cudaError_t launch_set_means(const double* src, int k, int d, FinalArgs f, int from_partition, long long n,
