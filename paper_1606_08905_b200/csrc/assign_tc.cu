@@ -534,7 +534,12 @@ __global__ void tc_prep_kernel(const double* __restrict__ means, const double* _
   const long long tot = (long long)kp * dp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(i / dp), e = (int)(i - (long long)j * dp);
-    c32[i] = (j < k && e < d) ? (float)means[(long long)j * d + e] : 0.0f;
+    // the B operand pre-rounded to TF32 (nearest): the tensor core's truncation of it is
+    // then exact, and only the row operand's truncation remains in the certificate
+    float v = (j < k && e < d) ? (float)means[(long long)j * d + e] : 0.0f;
+    uint32_t t;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
+    c32[i] = __uint_as_float(t);
     if (e == 0) chn32[j] = j < k ? (float)(-0.5 * cn2[j]) : -CUDART_INF_F;
   }
 }
