@@ -99,12 +99,14 @@ struct Scored {
 // Each lane returns the result for its row owner_lane^-1(lane) = t4*8 + g.
 // SMALLK: at most two 8-centroid tiles (k <= 16) -- one step, no software pipeline, so
 // the second set of accumulators never needs registers
-template <int DP, bool SMALLK = false>
+// LEAN: fewest registers (A fragments re-read from shared memory, one accumulator set,
+// tiles scored one step at a time) for kernels that trade them for more warps
+template <int DP, bool SMALLK = false, bool LEAN = false>
 __device__ __forceinline__ Scored score_block(const unsigned char* tb, const double* bf, const double* chn,
                                               int ntile8, double tolk, double cmax2, int lane) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;
-  constexpr bool ACACHE = DP <= 32;
+  constexpr bool ACACHE = DP <= 32 && !LEAN;
   const int g = lane >> 2, t4 = lane & 3;
   double afr[4][ACACHE ? KS : 1];
   double xn2[4];
@@ -185,6 +187,13 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
   mma_step(0, ca0, ca1);
   if constexpr (SMALLK) {
     epilogue(0, ca0, ca1);
+  } else if constexpr (LEAN) {
+    epilogue(0, ca0, ca1);
+#pragma unroll 1
+    for (int q = 2; q < ntile8; q += 2) {
+      mma_step(q, ca0, ca1);
+      epilogue(q, ca0, ca1);
+    }
   } else {
     double cb0[4][2], cb1[4][2];
     int q = 0;

@@ -35,8 +35,8 @@ __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / 
 struct MtiMmaSmem {
   size_t bf, crow, chn, hmin, drift, red, warp0, tile_off, tile_stride, q_off, acc_off, cnt_off, sq_off, per_warp,
       total;
-  // src: semi-external runs also queue each row's HBM cache slot
-  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W, bool src = false) {
+  // src: semi-external runs also queue each row's HBM cache slot; lean: one staging tile
+  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W, bool src = false, bool lean = false) {
     const int kp = (k + 7) & ~7;
     size_t o = 0;
     bf = o;    o += (size_t)kp * DP * 8;
@@ -44,12 +44,12 @@ struct MtiMmaSmem {
     chn = o;   o += (size_t)kp * 8;
     hmin = o;  o += (size_t)k * 8;
     drift = o; o += (size_t)k * 8;
-    red = o;   o += KNB_WARPS * 8 * 8;
+    red = o;   o += 16 * 8 * 8;
     o = al(o, 1024);
     warp0 = o;
     size_t w = 0;
     tile_stride = (size_t)BR * DP * 8;
-    tile_off = w; w += 2 * tile_stride;  // two staging tiles (gather double buffer)
+    tile_off = w; w += (lean ? 1 : 2) * tile_stride;  // staging tiles (gather double buffer)
     q_off = w;    w += 192 * 4 * (src ? 3 : 2);  // queued rows, pre-scan assignment (, cache slot)
     acc_off = w;  w += (size_t)k * d * 8;
     cnt_off = w;  w += (size_t)k * 8;
@@ -59,14 +59,21 @@ struct MtiMmaSmem {
   }
 };
 
+#ifndef KNB_MTI_LEAN
+#define KNB_MTI_LEAN 1
+#endif
+#ifndef KNB_LEAN_WARPS
+#define KNB_LEAN_WARPS 8
+#endif
 #ifndef KNB_MTI_2CTA_DP
 #define KNB_MTI_2CTA_DP 8
 #endif
 
 // HOST: rows in host memory (row_gather) and/or the semi-external HBM row cache; the
 // HBM-resident instantiation keeps the plain per-lane gather
-template <int DP, bool HOST, bool SMALLK>
-__global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1) mti_mma_kernel(const MtiArgs a) {
+template <int DP, bool HOST, bool SMALLK, bool LEAN>
+__global__ void __launch_bounds__(LEAN ? 32 * KNB_LEAN_WARPS : KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1)
+    mti_mma_kernel(const MtiArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -78,7 +85,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
   const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
   const int32_t* cslot = HOST ? a.cslot : nullptr;
-  const MtiMmaSmem L(DP, k, d, W, cslot != nullptr);
+  const MtiMmaSmem L(DP, k, d, W, cslot != nullptr, LEAN);
   double* bf = reinterpret_cast<double*>(smem + L.bf);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
   double* chn = reinterpret_cast<double*>(smem + L.chn);
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
 
   // score and update the first `cnum` queued survivors (cnum <= 32), staged in tb
   auto process = [&](const unsigned char* tb, int cnum) {
-    const Scored sc = score_block<DP, SMALLK>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+    const Scored sc = score_block<DP, SMALLK, LEAN>(tb, bf, chn, ntile8, tolk, cmax2, lane);
     const int r = t4 * 8 + g;
     const bool valid = r < cnum;
     int id = sc.id;
@@ -257,6 +264,21 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
     }
   };
 
+  if constexpr (LEAN) {
+    // one staging tile; the next batch is filtered while this one's rows arrive
+    filter_until(32);
+    int b0 = qn < 32 ? qn : 32;
+    while (b0 > 0) {
+      gather(tb, 0, b0);
+      filter_until(64);
+      cp_async_wait_all();
+      __syncwarp();
+      process(tb, b0);
+      qh = ring(b0);
+      qn -= b0;
+      b0 = qn < 32 ? qn : 32;
+    }
+  } else {
   // two staging tiles: the next batch's rows stream in while the current one is scored
   int cur = 0;
   filter_until(32);
@@ -280,6 +302,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
     qn = rest;
     b0 = b1;
     cur ^= 1;
+  }
   }
   __syncthreads();
 
@@ -312,28 +335,33 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
 
 constexpr size_t SMEM_MAX = 227 * 1024;
 
-int mti_warps_for(int DP, int k, int d, bool src = false) {
-  for (int W = KNB_WARPS; W >= 1; --W)
-    if (MtiMmaSmem(DP, k, d, W, src).total <= SMEM_MAX) return W;
+int mti_warps_for(int DP, int k, int d, bool src = false, bool lean = false) {
+  for (int W = lean ? KNB_LEAN_WARPS : KNB_WARPS; W >= 1; --W)
+    if (MtiMmaSmem(DP, k, d, W, src, lean).total <= SMEM_MAX) return W;
   return 0;
 }
 
-template <int DP, bool HOST, bool SMALLK>
+template <int DP, bool HOST, bool SMALLK, bool LEAN = false>
 cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
   const bool src = HOST && a.cslot != nullptr;
-  const int W = mti_warps_for(DP, a.k, a.d, src);
+  const int W = mti_warps_for(DP, a.k, a.d, src, LEAN);
   if (!W) return cudaErrorInvalidValue;
-  const MtiMmaSmem L(DP, a.k, a.d, W, src);
+  const MtiMmaSmem L(DP, a.k, a.d, W, src, LEAN);
   cudaError_t e =
-      cudaFuncSetAttribute(mti_mma_kernel<DP, HOST, SMALLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      cudaFuncSetAttribute(mti_mma_kernel<DP, HOST, SMALLK, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)L.total);
   if (e != cudaSuccess) return e;
-  return launch_pdl(mti_mma_kernel<DP, HOST, SMALLK>, dim3(grid), dim3(W * 32), L.total, s, a);
+  return launch_pdl(mti_mma_kernel<DP, HOST, SMALLK, LEAN>, dim3(grid), dim3(W * 32), L.total, s, a);
 }
 
 template <int DP>
 cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
   if (a.row_gather || a.cslot) return launch_host<DP, true, false>(a, grid, s);
-  return a.k <= 16 ? launch_host<DP, false, true>(a, grid, s) : launch_host<DP, false, false>(a, grid, s);
+  if (a.k <= 16) return launch_host<DP, false, true>(a, grid, s);
+#if KNB_MTI_LEAN
+  if constexpr (DP == 32) return launch_host<DP, false, false, true>(a, grid, s);
+#endif
+  return launch_host<DP, false, false>(a, grid, s);
 }
 
 }  // namespace
