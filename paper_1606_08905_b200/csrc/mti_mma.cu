@@ -35,8 +35,8 @@ __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / 
 struct MtiMmaSmem {
   size_t bf, crow, chn, hmin, drift, red, warp0, tile_off, tile_stride, q_off, acc_off, cnt_off, sq_off, per_warp,
       total;
-  // src: semi-external runs also queue each row's HBM cache slot; lean: one staging tile
-  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W, bool src = false, bool lean = false) {
+  // src: semi-external runs also queue each row's HBM cache slot
+  __host__ __device__ MtiMmaSmem(int DP, int k, int d, int W, bool src = false) {
     const int kp = (k + 7) & ~7;
     size_t o = 0;
     bf = o;    o += (size_t)kp * DP * 8;
@@ -49,7 +49,7 @@ struct MtiMmaSmem {
     warp0 = o;
     size_t w = 0;
     tile_stride = (size_t)BR * DP * 8;
-    tile_off = w; w += (lean ? 1 : 2) * tile_stride;  // staging tiles (gather double buffer)
+    tile_off = w; w += 2 * tile_stride;  // two staging tiles (gather double buffer)
     q_off = w;    w += 192 * 4 * (src ? 3 : 2);  // queued rows, pre-scan assignment (, cache slot)
     acc_off = w;  w += (size_t)k * d * 8;
     cnt_off = w;  w += (size_t)k * 8;
@@ -59,20 +59,17 @@ struct MtiMmaSmem {
   }
 };
 
-#ifndef KNB_MTI_LEAN
-#define KNB_MTI_LEAN 1
-#endif
-#ifndef KNB_LEAN_WARPS
-#define KNB_LEAN_WARPS 8
-#endif
 #ifndef KNB_MTI_2CTA_DP
 #define KNB_MTI_2CTA_DP 8
 #endif
 
+// LEAN (DP = 32): the scorer's fewest-register form -- measured 3% faster at c2 (the
+// registers go to scheduling freedom; twelve warps per CTA would cap them at 168 and
+// spill, and one staging tile instead of two is slower)
 // HOST: rows in host memory (row_gather) and/or the semi-external HBM row cache; the
 // HBM-resident instantiation keeps the plain per-lane gather
 template <int DP, bool HOST, bool SMALLK, bool LEAN>
-__global__ void __launch_bounds__(LEAN ? 32 * KNB_LEAN_WARPS : KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1)
+__global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1)
     mti_mma_kernel(const MtiArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;
@@ -85,7 +82,7 @@ __global__ void __launch_bounds__(LEAN ? 32 * KNB_LEAN_WARPS : KNB_NT, (SMALLK &
   const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
   const int32_t* cslot = HOST ? a.cslot : nullptr;
-  const MtiMmaSmem L(DP, k, d, W, cslot != nullptr, LEAN);
+  const MtiMmaSmem L(DP, k, d, W, cslot != nullptr);
   double* bf = reinterpret_cast<double*>(smem + L.bf);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
   double* chn = reinterpret_cast<double*>(smem + L.chn);
@@ -264,21 +261,6 @@ __global__ void __launch_bounds__(LEAN ? 32 * KNB_LEAN_WARPS : KNB_NT, (SMALLK &
     }
   };
 
-  if constexpr (LEAN) {
-    // one staging tile; the next batch is filtered while this one's rows arrive
-    filter_until(32);
-    int b0 = qn < 32 ? qn : 32;
-    while (b0 > 0) {
-      gather(tb, 0, b0);
-      filter_until(64);
-      cp_async_wait_all();
-      __syncwarp();
-      process(tb, b0);
-      qh = ring(b0);
-      qn -= b0;
-      b0 = qn < 32 ? qn : 32;
-    }
-  } else {
   // two staging tiles: the next batch's rows stream in while the current one is scored
   int cur = 0;
   filter_until(32);
@@ -302,7 +284,6 @@ __global__ void __launch_bounds__(LEAN ? 32 * KNB_LEAN_WARPS : KNB_NT, (SMALLK &
     qn = rest;
     b0 = b1;
     cur ^= 1;
-  }
   }
   __syncthreads();
 
@@ -335,18 +316,18 @@ __global__ void __launch_bounds__(LEAN ? 32 * KNB_LEAN_WARPS : KNB_NT, (SMALLK &
 
 constexpr size_t SMEM_MAX = 227 * 1024;
 
-int mti_warps_for(int DP, int k, int d, bool src = false, bool lean = false) {
-  for (int W = lean ? KNB_LEAN_WARPS : KNB_WARPS; W >= 1; --W)
-    if (MtiMmaSmem(DP, k, d, W, src, lean).total <= SMEM_MAX) return W;
+int mti_warps_for(int DP, int k, int d, bool src = false) {
+  for (int W = KNB_WARPS; W >= 1; --W)
+    if (MtiMmaSmem(DP, k, d, W, src).total <= SMEM_MAX) return W;
   return 0;
 }
 
 template <int DP, bool HOST, bool SMALLK, bool LEAN = false>
 cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
   const bool src = HOST && a.cslot != nullptr;
-  const int W = mti_warps_for(DP, a.k, a.d, src, LEAN);
+  const int W = mti_warps_for(DP, a.k, a.d, src);
   if (!W) return cudaErrorInvalidValue;
-  const MtiMmaSmem L(DP, a.k, a.d, W, src, LEAN);
+  const MtiMmaSmem L(DP, a.k, a.d, W, src);
   cudaError_t e =
       cudaFuncSetAttribute(mti_mma_kernel<DP, HOST, SMALLK, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)L.total);
@@ -358,9 +339,7 @@ template <int DP>
 cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
   if (a.row_gather || a.cslot) return launch_host<DP, true, false>(a, grid, s);
   if (a.k <= 16) return launch_host<DP, false, true>(a, grid, s);
-#if KNB_MTI_LEAN
   if constexpr (DP == 32) return launch_host<DP, false, false, true>(a, grid, s);
-#endif
   return launch_host<DP, false, false>(a, grid, s);
 }
 
