@@ -101,7 +101,10 @@ struct Scored {
 // the second set of accumulators never needs registers
 // LEAN: fewest registers (A fragments re-read from shared memory, one accumulator set,
 // tiles scored one step at a time) for kernels that trade them for more warps
-template <int DP, bool SMALLK = false, bool LEAN = false>
+// BCROW: `bf` is the row-major centroid copy with stride crow_stride<DP>() instead of
+// the fragment-ordered array (saves kp x DP x 8 bytes of shared memory; the 8 rows x 32
+// bytes of one fragment load still take the minimum two wavefronts at that stride)
+template <int DP, bool SMALLK = false, bool LEAN = false, bool BCROW = false>
 __device__ __forceinline__ Scored score_block(const unsigned char* tb, const double* bf, const double* chn,
                                               int ntile8, double tolk, double cmax2, int lane) {
   using TL = TileLayout<DP>;
@@ -153,8 +156,14 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
     const int q1 = two ? q + 1 : q;  // a valid fragment address for the dummy tile
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      const double bv0 = bf[((q * KS + ks) << 5) + lane];
-      const double bv1 = bf[((q1 * KS + ks) << 5) + lane];
+      double bv0, bv1;
+      if constexpr (BCROW) {
+        bv0 = bf[(q * 8 + g) * crow_stride<DP>() + ks * 4 + t4];
+        bv1 = bf[(q1 * 8 + g) * crow_stride<DP>() + ks * 4 + t4];
+      } else {
+        bv0 = bf[((q * KS + ks) << 5) + lane];
+        bv1 = bf[((q1 * KS + ks) << 5) + lane];
+      }
 #pragma unroll
       for (int pg = 0; pg < 4; ++pg) {
         double av;
@@ -259,6 +268,73 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
   }
   if (sq_out) *sq_out = exact_sq<DP>(x, Zero{}, d);
   return nd;
+}
+
+// exact_sq_fixed<DP> (d == DP, DP in {16, 32, 64}) streamed: x from tile row r, c from a
+// crow row, eight elements at a time in the tree's own grouping (group a of every
+// 32-element block feeds z[a][*], then acc[a][l] = z[a][l] + z[a][l + 4] joins s[l] in
+// the order ((acc0 + acc1) + acc2) + acc3) -- the same roundings in the same order,
+// with about 20 doubles live instead of the whole row and centroid
+// SELF: c = 0 (row_sqnorms' vecdot(x, x): x - 0.0 == x, the same tree)
+template <int DP, bool SELF = false>
+__device__ __forceinline__ double exact_sq_stream(const unsigned char* tb, int r, const double* __restrict__ c) {
+  static_assert(DP == 16 || DP == 32 || DP == 64, "streamed tree for d == DP in {16, 32, 64}");
+  using TL = TileLayout<DP>;
+  constexpr int n32 = DP & ~31;
+  double s[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double acc[4];
+    if constexpr (n32 > 0) {
+      double z[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) z[l] = 0.0;
+#pragma unroll
+      for (int i = 0; i < n32; i += 32) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int e = i + 8 * a + 2 * h;
+          const double2 xv = *reinterpret_cast<const double2*>(tb + TL::chunk_off(r, e >> 1, BR));
+          const double2 cv = SELF ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(c + e);
+          const double v0 = __dsub_rn(xv.x, cv.x), v1 = __dsub_rn(xv.y, cv.y);
+          z[2 * h] = __fma_rn(v0, v0, z[2 * h]);
+          z[2 * h + 1] = __fma_rn(v1, v1, z[2 * h + 1]);
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) acc[l] = __dadd_rn(z[l], z[l + 4]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = 4 * a + 2 * h;
+        const double2 xv = *reinterpret_cast<const double2*>(tb + TL::chunk_off(r, e >> 1, BR));
+        const double2 cv = SELF ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(c + e);
+        const double v0 = __dsub_rn(xv.x, cv.x), v1 = __dsub_rn(xv.y, cv.y);
+        acc[2 * h] = __fma_rn(v0, v0, 0.0);
+        acc[2 * h + 1] = __fma_rn(v1, v1, 0.0);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) s[l] = a == 0 ? acc[l] : __dadd_rn(s[l], acc[l]);
+  }
+  return __dadd_rn(__dadd_rn(s[0], s[2]), __dadd_rn(s[1], s[3]));
+}
+
+// exact_winner for d == DP with the streamed tree (fewest registers)
+template <int DP>
+__device__ __forceinline__ double exact_winner_stream(const unsigned char* tb, int r, const double* crow, int k,
+                                                      bool flag, int& id) {
+  if (flag) {
+    double bd = CUDART_INF;
+    int bi = 0;
+    for (int j = 0; j < k; ++j) {
+      const double dj = sqrt(exact_sq_stream<DP>(tb, r, crow + j * crow_stride<DP>()));
+      if (dj < bd) { bd = dj; bi = j; }
+    }
+    id = bi;
+    return bd;
+  }
+  return sqrt(exact_sq_stream<DP>(tb, r, crow + id * crow_stride<DP>()));
 }
 
 // vecdot(x, x) of tile row r by the exact recipe (row_sqnorms, distance.py:66-72)

@@ -314,7 +314,216 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Twelve-warp form (rows in HBM, d == DP): the same filter / gather / certified DMMA
+// scoring / exact bound / signed deltas as mti_mma_kernel, re-budgeted so that three
+// warps share each SMSP instead of two -- the pass is bound by warp-level latency, not by
+// the tensor pipe (profiles/README.md).  Per warp: one staging tile (the next batch is
+// gathered while the following one is filtered), a 160-entry queue; per CTA: one
+// row-major centroid copy serving both the B fragments and the exact recipe; the exact
+// distances stream through the tree eight elements at a time (about 20 live doubles).
+constexpr int W12_Q = 160;  // < 32 queued + one group of FB = 4 blocks
+
+struct MtiW12Smem {
+  size_t crow, chn, hd, red, warp0, tile_stride, q_off, acc_off, cnt_off, sq_off, per_warp, total;
+  __host__ __device__ MtiW12Smem(int DP, int k, int d, int W) {
+    const int kp = (k + 7) & ~7;
+    size_t o = 0;
+    crow = o;  o += (size_t)kp * (DP + 2) * 8;
+    chn = o;   o += (size_t)kp * 8;
+    hd = o;    o += (size_t)k * 16;  // {drift, half_min}
+    red = o;   o += 16 * 8 * 8;
+    o = al(o, 128);
+    warp0 = o;
+    size_t w = 0;
+    tile_stride = (size_t)BR * DP * 8;
+    w += tile_stride;
+    q_off = w;    w += W12_Q * 4 * 2;
+    acc_off = w;  w += (size_t)k * d * 8;
+    cnt_off = w;  w += (size_t)k * 8;
+    sq_off = w;   w += (size_t)k * 8;
+    per_warp = al(w, 128);
+    total = warp0 + (size_t)W * per_warp;
+  }
+};
+
+#ifndef KNB_W12_THREADS
+#define KNB_W12_THREADS 384
+#endif
+
+template <int DP>
+__global__ void __launch_bounds__(KNB_W12_THREADS, 1) mti_w12_kernel(const MtiArgs a) {
+  using TL = TileLayout<DP>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  pdl_enter();
+  if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
+  if (a.gate && a.ctrl->mti_choice != 0) return;  // the block-dense pass runs this iteration
+  const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
+  const MtiW12Smem L(DP, k, d, W);
+  double* crow = reinterpret_cast<double*>(smem + L.crow);
+  double* chn = reinterpret_cast<double*>(smem + L.chn);
+  double2* hd = reinterpret_cast<double2*>(smem + L.hd);
+  double* red = reinterpret_cast<double*>(smem + L.red);
+  unsigned char* wbase = smem + L.warp0 + (size_t)warp * L.per_warp;
+  unsigned char* tb = wbase;
+  int* qrow = reinterpret_cast<int*>(wbase + L.q_off);
+  int* qorig = qrow + W12_Q;
+  int qh = 0;
+  auto ring = [&](int i) { const int x = qh + i; return x >= W12_Q ? x - W12_Q : x; };
+  double* acc = reinterpret_cast<double*>(wbase + L.acc_off);
+  double* cnt = reinterpret_cast<double*>(wbase + L.cnt_off);
+  double* sqa = reinterpret_cast<double*>(wbase + L.sq_off);
+
+  for (int i = tid; i < kp * DP; i += blockDim.x) {
+    const int j = i / DP, e = i - j * DP;
+    crow[j * crow_stride<DP>() + e] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
+  }
+  for (int j = tid; j < kp; j += blockDim.x) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
+  for (int j = tid; j < k; j += blockDim.x) hd[j] = make_double2(a.drift[j], a.half_min[j]);
+  for (int i = lane; i < k * d + 2 * k; i += 32) acc[i] = 0.0;  // acc, cnt, sq are contiguous
+  // rows past a batch keep stale finite data (d == DP: no padded dims)
+  for (int i = lane; i < BR * DP; i += 32) reinterpret_cast<double*>(tb)[i] = 0.0;
+  __syncthreads();
+
+  const double cmax2 = a.ctrl->cmax2;
+  const double tolk = (8.0 * d + 32.0) * 1.1102230246251565e-16;
+  const long long nblk = (a.n + BR - 1) / BR;
+  const long long gw = (long long)blockIdx.x * W + warp, TW = (long long)gridDim.x * W;
+  long long skips = 0, computed = 0, reassigned = 0;
+  int qn = 0;
+
+  // async gather of queued entries [0, cnum) into the staging tile: every lane its row
+  auto gather = [&](int cnum) {
+    const uint32_t dst = smem_u32(tb);
+    if (lane < cnum) {
+      const double* src = a.X + (long long)qrow[ring(lane)] * d;
+#pragma unroll
+      for (int q2 = 0; q2 < DP / 2; ++q2) cp_async16_s(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
+    }
+    cp_async_commit();
+  };
+
+  long long blk = gw;
+  constexpr int FB = 4;
+  auto filter_until = [&](int target) {
+    while (qn < target && blk < nblk) {
+      int aa[FB];
+      double uu[FB];
+#pragma unroll
+      for (int j = 0; j < FB; ++j) {
+        const long long row = (blk + j * TW) * BR + lane;
+        const bool ok = blk + j * TW < nblk && row < a.n;
+        aa[j] = ok ? a.assign[row] : -1;
+        uu[j] = ok ? a.upper[row] : 0.0;
+      }
+      const long long cur = blk;
+      blk += FB * TW;
+#pragma unroll
+      for (int j = 0; j < FB; ++j) {
+        if (cur + j * TW >= nblk) break;  // uniform
+        const long long row = (cur + j * TW) * BR + lane;
+        bool live = false;
+        if (aa[j] >= 0) {
+          const double2 dh = hd[aa[j]];
+          const double u = uu[j] + dh.x;  // u + 0.0 == u
+          if (u <= dh.y) {
+            ++skips;
+            if (dh.x != 0.0) {  // the inflated bound is the skipped row's final state
+              a.upper[row] = u;
+              a.tight[row] = 0;
+            }
+          } else {
+            live = true;  // a survivor's bound and tight flag are rewritten by its scan
+          }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, live);
+        if (live) {
+          const int pos = ring(qn + __popc(b & ((1u << lane) - 1u)));
+          qrow[pos] = (int)row;
+          qorig[pos] = aa[j];
+        }
+        qn += __popc(b);
+      }
+      __syncwarp();
+    }
+  };
+
+  // batch loop: gather the next 32 survivors, filter ahead while they land, score
+  filter_until(32);
+  while (qn > 0) {
+    const int cnum = qn < 32 ? qn : 32;
+    gather(cnum);
+    filter_until(32 + cnum);  // the following batch's survivors, overlapping the gather
+    cp_async_wait_all();
+    __syncwarp();
+    const Scored sc = score_block<DP, false, true, true>(tb, crow, chn, ntile8, tolk, cmax2, lane);
+    const int r = t4 * 8 + g;
+    const bool valid = r < cnum;
+    int id = sc.id;
+    const double nd = exact_winner_stream<DP>(tb, r, crow, k, sc.flag, id);
+    const int orig = valid ? qorig[ring(r)] : 0;
+    const bool moved = valid && id != orig;
+    const double sq = moved ? exact_sq_stream<DP, true>(tb, r, nullptr) : 0.0;
+    if (valid) {
+      const long long grow = qrow[ring(r)];
+      a.upper[grow] = nd;
+      a.tight[grow] = 1;
+      if (moved) {
+        a.assign[grow] = id;
+        ++reassigned;
+      }
+    }
+    if (lane == 0) computed += (long long)cnum * k;
+    accumulate_in_row_order<DP>(row_mask(moved, r), id, orig, sq, tb, acc, cnt, sqa, d, lane);
+    __syncwarp();
+    qh = ring(cnum);  // pop the batch
+    qn -= cnum;
+  }
+  __syncthreads();
+
+  const long long Lg = acc_len(k, d);
+  double* out = a.partials + (long long)blockIdx.x * Lg;
+  const long long kd = (long long)k * d;
+  for (long long i = tid; i < kd + 2LL * k; i += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < W; ++w) v += reinterpret_cast<const double*>(smem + L.warp0 + (size_t)w * L.per_warp + L.acc_off)[i];
+    out[i] = v;
+  }
+  const long long v0 = warp_sum_ll(reassigned), v1 = warp_sum_ll(computed), v2 = warp_sum_ll(skips);
+  if (lane == 0) { red[warp * 8 + 0] = (double)v0; red[warp * 8 + 1] = (double)v1; red[warp * 8 + 2] = (double)v2; }
+  __syncthreads();
+  if (tid == 0) {
+    double t0 = 0, t1 = 0, t2 = 0;
+    for (int w = 0; w < W; ++w) { t0 += red[w * 8]; t1 += red[w * 8 + 1]; t2 += red[w * 8 + 2]; }
+    double* sc = out + kd + 2LL * k;
+    for (int i = 0; i < NSCAL; ++i) sc[i] = 0.0;
+    sc[S_REASSIGNED] = t0;
+    sc[S_COMPUTED] = t1;
+    sc[S_SKIPS] = t2;
+  }
+}
+
 constexpr size_t SMEM_MAX = 227 * 1024;
+
+int w12_warps_for(int DP, int k, int d) {
+  if (d != DP || (DP != 16 && DP != 32)) return 0;
+  for (int W = KNB_W12_THREADS / 32; W >= 9; --W)
+    if (MtiW12Smem(DP, k, d, W).total <= SMEM_MAX) return W;
+  return 0;  // fewer than nine warps: the two-tile kernel is the better trade
+}
+
+template <int DP>
+cudaError_t launch_w12(const MtiArgs& a, int grid, cudaStream_t s) {
+  const int W = w12_warps_for(DP, a.k, a.d);
+  const MtiW12Smem L(DP, a.k, a.d, W);
+  cudaError_t e =
+      cudaFuncSetAttribute(mti_w12_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(mti_w12_kernel<DP>, dim3(grid), dim3(W * 32), L.total, s, a);
+}
 
 int mti_warps_for(int DP, int k, int d, bool src = false) {
   for (int W = KNB_WARPS; W >= 1; --W)
@@ -338,6 +547,11 @@ cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
 template <int DP>
 cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
   if (a.row_gather || a.cslot) return launch_host<DP, true, false>(a, grid, s);
+  if constexpr (DP == 16 || DP == 32) {
+    // (KNB_MTI_W12=0: the two-tile eight-warp kernel, for A/B measurements)
+    static const int w12_env = [] { const char* v = getenv("KNB_MTI_W12"); return v ? atoi(v) : 1; }();
+    if (w12_env && a.k > 16 && w12_warps_for(DP, a.k, a.d)) return launch_w12<DP>(a, grid, s);
+  }
   if (a.k <= 16) return launch_host<DP, false, true>(a, grid, s);
   if constexpr (DP == 32) return launch_host<DP, false, false, true>(a, grid, s);
   return launch_host<DP, false, false>(a, grid, s);
