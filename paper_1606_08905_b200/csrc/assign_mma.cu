@@ -48,21 +48,22 @@ namespace {
 
 __host__ __device__ inline size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-__host__ __device__ inline int stages_for(int DP) { return DP <= 8 ? 4 : 2; }
+// W12: the twelve-warp budget (one stage per warp, no fragment-ordered copy)
+__host__ __device__ constexpr int stages_for(int DP, bool w12 = false) { return w12 ? 1 : DP <= 8 ? 4 : 2; }
 
 // shared memory: [centroids: bf, crow, chn] [per warp: NS stages, mbar, acc, cnt, sq]
 struct WarpSmem {
   size_t bf, crow, chn, hmin, drift, warp0, stage_bytes, mbar_off, acc_off, cnt_off, sq_off, per_warp, red, total;
-  __host__ __device__ WarpSmem(int DP, int k, int d, int W) {
+  __host__ __device__ WarpSmem(int DP, int k, int d, int W, bool w12 = false) {
     const int kp = (k + 7) & ~7;
-    const int NS = stages_for(DP);
+    const int NS = stages_for(DP, w12);
     size_t o = 0;
-    bf = o;   o += (size_t)kp * DP * 8;
+    bf = o;   o += w12 ? 0 : (size_t)kp * DP * 8;
     crow = o; o += (size_t)kp * (DP + 2) * 8;
     chn = o;  o += (size_t)kp * 8;
     hmin = o; o += (size_t)k * 8;
     drift = o; o += (size_t)k * 8;
-    red = o;  o += KNB_WARPS * 8 * 8;
+    red = o;  o += 16 * 8 * 8;
     o = al(o, 1024);
     warp0 = o;
     stage_bytes = (size_t)BR * DP * 8;              // multiple of 1024 for DP >= 4
@@ -114,12 +115,19 @@ __device__ __forceinline__ void load_block(const CUtensorMap* tmap, uint64_t* ba
 
 // SMALLK (k <= 16): the scorer's one-step form; with narrow rows it leaves room for
 // two CTAs per SM (<= 128 registers, no spills)
-template <int DP, bool SMALLK>
-__global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 2 : 1)
+// W12 (d == DP in {16, 32}, k > 16): up to twelve warps per SM at <= 168 registers --
+// one TMA stage per warp (the next block is prefetched into L2 while the current one is
+// scored), B fragments from the row-major centroid copy, exact distances streamed
+// through the tree; the pass is bound by warp-level latency (profiles/README.md)
+#ifndef KNB_DENSE_W12_THREADS
+#define KNB_DENSE_W12_THREADS 384
+#endif
+template <int DP, bool SMALLK, bool W12 = false>
+__global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 2 : 1)
     dense_mma_kernel(const __grid_constant__ CUtensorMap tmap, const DenseArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;         // k-steps of 4 dims
-  constexpr int NS = DP <= 8 ? 4 : 2;
+  constexpr int NS = stages_for(DP, W12);
   extern __shared__ __align__(1024) unsigned char smem[];
   pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
   const int W = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
-  const WarpSmem L(DP, k, d, W);
+  const WarpSmem L(DP, k, d, W, W12);
   double* hmin_s = reinterpret_cast<double*>(smem + L.hmin);
   double* drift_s = reinterpret_cast<double*>(smem + L.drift);
   double* bf = reinterpret_cast<double*>(smem + L.bf);
@@ -149,9 +157,11 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
   for (int i = tid; i < kp * DP; i += blockDim.x) {
     const int j = i / DP, e = i - j * DP;
     crow[j * crow_stride<DP>() + e] = (j < k && e < d) ? a.means[(long long)j * d + e] : 0.0;
-    const int l = i & 31, qs = i >> 5, q = qs / KS, s = qs - q * KS;
-    const int jb = q * 8 + (l >> 2), eb = s * 4 + (l & 3);
-    bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
+    if constexpr (!W12) {
+      const int l = i & 31, qs = i >> 5, q = qs / KS, s = qs - q * KS;
+      const int jb = q * 8 + (l >> 2), eb = s * 4 + (l & 3);
+      bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
+    }
   }
   for (int j = tid; j < kp; j += blockDim.x) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
   if (a.mti_filter)
@@ -204,13 +214,21 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
     const int s = it % NS;
     unsigned char* tb = wbase + s * L.stage_bytes;
     if (tma) {
+      if constexpr (W12) {  // one stage: the next block heads for L2 while this one is scored
+        const long long pb = blk + TW;
+        if (lane == 0 && pb < nblk) {
+#pragma unroll
+          for (int p = 0; p < TL::NPANEL; ++p) tma_prefetch_l2_2d(&tmap, p * TL::PW, (int)(pb * BR));
+        }
+      }
       mbar_wait(&bar[s], (uint32_t)((it / NS) & 1));
     } else {
       // groups complete in order: allow the NS-1 younger groups to stay in flight
       const long long left = (nblk - 1 - blk) / TW;  // blocks after this one
       if (left >= NS - 1) {
         if constexpr (NS == 4) asm volatile("cp.async.wait_group 3;" ::: "memory");
-        else asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else if constexpr (NS == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else cp_async_wait_all();
       } else {
         cp_async_wait_all();
       }
@@ -239,10 +257,16 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
       skips += (valid && !live) ? 1 : 0;
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
       if (lmask) {
-        const Scored sc = score_block<DP, SMALLK>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+        const Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
         int nid = sc.id;
-        const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr);
-        const double sq = (live && nid != aa) ? row_self_sq<DP>(tb, my_r, d) : 0.0;
+        double nd, sq = 0.0;
+        if constexpr (W12) {
+          nd = exact_winner_stream<DP>(tb, my_r, crow, k, sc.flag, nid);
+          if (live && nid != aa) sq = exact_sq_stream<DP, true>(tb, my_r, nullptr);
+        } else {
+          nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr);
+          if (live && nid != aa) sq = row_self_sq<DP>(tb, my_r, d);
+        }
         if (live) {
           a.upper[row] = nd;
           a.tight[row] = 1;
@@ -255,12 +279,18 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
         accumulate_in_row_order<DP>(row_mask(live && nid != aa, my_r), nid, aa, sq, tb, acc, cnt, sqa, d, lane);
       }
     } else if (!labels) {
-      const Scored sc = score_block<DP, SMALLK>(tb, bf, chn, ntile8, tolk, cmax2, lane);
+      const Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
       id = sc.id;
       double nd2;
       if (sc.flag || a.mti_seed) {
         // exact recipe: near-tie re-rank, or the MTI bound seed (engine.py:305-308)
-        const double nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, id, a.mti_seed ? &my_sq : nullptr);
+        double nd;
+        if constexpr (W12) {
+          nd = exact_winner_stream<DP>(tb, my_r, crow, k, sc.flag, id);
+          if (a.mti_seed) my_sq = exact_sq_stream<DP, true>(tb, my_r, nullptr);
+        } else {
+          nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, id, a.mti_seed ? &my_sq : nullptr);
+        }
         nd2 = nd * nd;
         if (a.mti_seed && valid) {
           a.upper[row] = nd;
@@ -350,25 +380,36 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 
 
 constexpr size_t SMEM_MAX = 227 * 1024;
 
-int warps_for(int DP, int k, int d) {
-  for (int W = KNB_WARPS; W >= 1; --W)
-    if (WarpSmem(DP, k, d, W).total <= SMEM_MAX) return W;
+int warps_for(int DP, int k, int d, bool w12 = false) {
+  for (int W = w12 ? KNB_DENSE_W12_THREADS / 32 : KNB_WARPS; W >= 1; --W)
+    if (WarpSmem(DP, k, d, W, w12).total <= SMEM_MAX) return W;
   return 0;
 }
 
-template <int DP, bool SMALLK>
+// the twelve-warp form when at least eleven warps fit (KNB_DENSE_W12=0: off, A/B runs).
+// Measured: c2 (d = 32, k = 32, 12 warps) 0.244 -> 0.220 ms per steady pass; c4 (d = 16,
+// k = 100: 10 warps, the sums take 13 KB per warp) 35.5 -> 37.5 ms per 200M rows, so
+// the two-stage eight-warp form stays there
+bool use_w12(int DP, int k, int d) {
+  static const int env = [] { const char* v = getenv("KNB_DENSE_W12"); return v ? atoi(v) : 1; }();
+  return env && d == DP && (DP == 16 || DP == 32) && k > 16 && warps_for(DP, k, d, true) >= 11;
+}
+
+template <int DP, bool SMALLK, bool W12 = false>
 cudaError_t launch_mma_k(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
-  const int W = warps_for(DP, a.k, a.d);
+  const int W = warps_for(DP, a.k, a.d, W12);
   if (!W) return cudaErrorInvalidValue;
-  const WarpSmem L(DP, a.k, a.d, W);
-  cudaError_t e =
-      cudaFuncSetAttribute(dense_mma_kernel<DP, SMALLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  const WarpSmem L(DP, a.k, a.d, W, W12);
+  cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<DP, SMALLK, W12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)L.total);
   if (e != cudaSuccess) return e;
-  return launch_pdl(dense_mma_kernel<DP, SMALLK>, dim3(grid), dim3(W * 32), L.total, s, *tmap, a);
+  return launch_pdl(dense_mma_kernel<DP, SMALLK, W12>, dim3(grid), dim3(W * 32), L.total, s, *tmap, a);
 }
 
 template <int DP>
 cudaError_t launch_mma_dp(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
+  if constexpr (DP == 16 || DP == 32)
+    if (use_w12(DP, a.k, a.d)) return launch_mma_k<DP, false, true>(tmap, a, grid, s);
   return a.k <= 16 ? launch_mma_k<DP, true>(tmap, a, grid, s) : launch_mma_k<DP, false>(tmap, a, grid, s);
 }
 
@@ -385,8 +426,9 @@ int dense_mma_dp(int d) {
 
 // 0 when even one warp's buffers do not fit (the generic kernel takes over)
 size_t dense_mma_smem(int DP, int k, int d) {
-  const int W = warps_for(DP, k, d);
-  return W ? WarpSmem(DP, k, d, W).total : (size_t)-1;
+  const bool w12 = use_w12(DP, k, d);
+  const int W = warps_for(DP, k, d, w12);
+  return W ? WarpSmem(DP, k, d, W, w12).total : (size_t)-1;
 }
 
 int dense_mma_rows() { return BR; }

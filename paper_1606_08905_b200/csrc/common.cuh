@@ -364,6 +364,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
       : "memory");
 }
 
+// 2-D tensor TMA prefetch of a box into L2 (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_l2_2d(const void* tmap, int col, int row) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tmap), "r"(col), "r"(row)
+               : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
