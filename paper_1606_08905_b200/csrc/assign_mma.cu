@@ -386,13 +386,13 @@ int warps_for(int DP, int k, int d, bool w12 = false) {
   return 0;
 }
 
-// the twelve-warp form when at least eleven warps fit (KNB_DENSE_W12=0: off, A/B runs).
+// the twelve-warp form when all twelve warps fit (KNB_DENSE_W12=0: off, A/B runs).
 // Measured: c2 (d = 32, k = 32, 12 warps) 0.244 -> 0.220 ms per steady pass; c4 (d = 16,
-// k = 100: 10 warps, the sums take 13 KB per warp) 35.5 -> 37.5 ms per 200M rows, so
+// k = 100: 11 warps, the sums take 13 KB per warp) 35.5 -> 37.5 ms per 200M rows, so
 // the two-stage eight-warp form stays there
 bool use_w12(int DP, int k, int d) {
   static const int env = [] { const char* v = getenv("KNB_DENSE_W12"); return v ? atoi(v) : 1; }();
-  return env && d == DP && (DP == 16 || DP == 32) && k > 16 && warps_for(DP, k, d, true) >= 11;
+  return env && d == DP && (DP == 16 || DP == 32) && k > 16 && warps_for(DP, k, d, true) >= 12;
 }
 
 template <int DP, bool SMALLK, bool W12 = false>

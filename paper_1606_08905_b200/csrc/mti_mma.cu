@@ -510,9 +510,8 @@ constexpr size_t SMEM_MAX = 227 * 1024;
 
 int w12_warps_for(int DP, int k, int d) {
   if (d != DP || (DP != 16 && DP != 32)) return 0;
-  for (int W = KNB_W12_THREADS / 32; W >= 9; --W)
-    if (MtiW12Smem(DP, k, d, W).total <= SMEM_MAX) return W;
-  return 0;  // fewer than nine warps: the two-tile kernel is the better trade
+  const int W = KNB_W12_THREADS / 32;
+  return MtiW12Smem(DP, k, d, W).total <= SMEM_MAX ? W : 0;  // else the two-tile kernel
 }
 
 template <int DP>
