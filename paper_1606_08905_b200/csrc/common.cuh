@@ -297,14 +297,20 @@ struct Zero {
 //   row bytes  64 -> SWIZZLE_64B : chunk ^= (r >> 1) & 3
 //   row bytes  32 -> SWIZZLE_32B : chunk ^= (r >> 2) & 1
 //   row bytes  16 -> no swizzle
-template <int DP>
+// SW = 1 (tiles written by cp.async, never by TMA): 128-byte rows use the chunk
+// permutation s(r) = 2 (r & 3) + ((r >> 2) & 1) instead of r & 7.  Both spread 8
+// consecutive rows over the 8 bank groups; s also spreads the DMMA A-fragment load
+// (a half-warp reads 4 rows x 2 adjacent chunks: {c ^ s(r)} hits 8 distinct groups,
+// where r & 7 hits 4 twice -- a 2-way conflict on every fragment load)
+template <int DP, int SW = 0>
 struct TileLayout {
   static constexpr int PW = DP < 16 ? DP : 16;      // doubles per panel row
   static constexpr int RB = PW * 8;                 // bytes per panel row
   static constexpr int NPANEL = DP / PW;
   static constexpr int CH = PW / 2;                 // 16-byte chunks per panel row
   __device__ static __forceinline__ int swz(int r) {
-    if constexpr (RB == 128) return r & 7;
+    if constexpr (RB == 128 && SW == 1) return ((r & 3) << 1) | ((r >> 2) & 1);
+    else if constexpr (RB == 128) return r & 7;
     else if constexpr (RB == 64) return (r >> 1) & 3;
     else if constexpr (RB == 32) return (r >> 2) & 1;
     else return 0;

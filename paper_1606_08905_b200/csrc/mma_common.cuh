@@ -87,6 +87,14 @@ __device__ __forceinline__ void combine(double& best, int& bid, bool& flag, int 
 // Lane that finishes row r of a block after the quad combine (row = t4*8 + g).
 __device__ __forceinline__ int owner_lane(int r) { return ((r & 7) << 2) | (r >> 3); }
 
+// Upper bound of ||x||^2 for a survivor of the MTI filter: u >= d(x, c_a) (the inflated
+// bound, exact recipe up to rounding) and ||c_a||^2 = -2 chn[a], so
+// ||x||^2 <= (||c_a|| + u)^2 <= 2 ||c_a||^2 + 2 u^2; the factor covers the rounding of
+// both terms (relative 1e-13 at most) with a wide margin.
+__device__ __forceinline__ double xnorm2_bound(double u, double chn_a) {
+  return (2.0 * u * u - 4.0 * chn_a) * (1.0 + 0x1p-30);
+}
+
 struct Scored {
   int id;       // certified argmax (or 0 when uncertified)
   bool flag;    // near tie: caller re-ranks with the exact recipe
@@ -104,10 +112,13 @@ struct Scored {
 // BCROW: `bf` is the row-major centroid copy with stride crow_stride<DP>() instead of
 // the fragment-ordered array (saves kp x DP x 8 bytes of shared memory; the 8 rows x 32
 // bytes of one fragment load still take the minimum two wavefronts at that stride)
-template <int DP, bool SMALLK = false, bool LEAN = false, bool BCROW = false>
+// XB: the caller knows an upper bound of ||x||^2 for every row (lane r holds row r's in
+// xb); the certificate only needs an upper bound, so the d-term sums are skipped.
+// TL: the staging tile's layout (TileLayout<DP> or its cp.async-only variant)
+template <int DP, bool SMALLK = false, bool LEAN = false, bool BCROW = false, bool XB = false,
+          class TL = TileLayout<DP>>
 __device__ __forceinline__ Scored score_block(const unsigned char* tb, const double* bf, const double* chn,
-                                              int ntile8, double tolk, double cmax2, int lane) {
-  using TL = TileLayout<DP>;
+                                              int ntile8, double tolk, double cmax2, int lane, double xb = 0.0) {
   constexpr int KS = DP / 4;
   constexpr bool ACACHE = DP <= 32 && !LEAN;
   const int g = lane >> 2, t4 = lane & 3;
@@ -115,6 +126,15 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
   double xn2[4];
 #pragma unroll
   for (int pg = 0; pg < 4; ++pg) {
+    if constexpr (XB) {
+      xn2[pg] = __shfl_sync(0xffffffffu, xb, pg * 8 + g);
+      if constexpr (ACACHE) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+          afr[pg][ks] = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
+      }
+      continue;
+    }
     double s2 = 0.0;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -276,10 +296,9 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
 // the order ((acc0 + acc1) + acc2) + acc3) -- the same roundings in the same order,
 // with about 20 doubles live instead of the whole row and centroid
 // SELF: c = 0 (row_sqnorms' vecdot(x, x): x - 0.0 == x, the same tree)
-template <int DP, bool SELF = false>
+template <int DP, bool SELF = false, class TL = TileLayout<DP>>
 __device__ __forceinline__ double exact_sq_stream(const unsigned char* tb, int r, const double* __restrict__ c) {
   static_assert(DP == 16 || DP == 32 || DP == 64, "streamed tree for d == DP in {16, 32, 64}");
-  using TL = TileLayout<DP>;
   constexpr int n32 = DP & ~31;
   double s[4];
 #pragma unroll
@@ -321,20 +340,20 @@ __device__ __forceinline__ double exact_sq_stream(const unsigned char* tb, int r
 }
 
 // exact_winner for d == DP with the streamed tree (fewest registers)
-template <int DP>
+template <int DP, class TL = TileLayout<DP>>
 __device__ __forceinline__ double exact_winner_stream(const unsigned char* tb, int r, const double* crow, int k,
                                                       bool flag, int& id) {
   if (flag) {
     double bd = CUDART_INF;
     int bi = 0;
     for (int j = 0; j < k; ++j) {
-      const double dj = sqrt(exact_sq_stream<DP>(tb, r, crow + j * crow_stride<DP>()));
+      const double dj = sqrt(exact_sq_stream<DP, false, TL>(tb, r, crow + j * crow_stride<DP>()));
       if (dj < bd) { bd = dj; bi = j; }
     }
     id = bi;
     return bd;
   }
-  return sqrt(exact_sq_stream<DP>(tb, r, crow + id * crow_stride<DP>()));
+  return sqrt(exact_sq_stream<DP, false, TL>(tb, r, crow + id * crow_stride<DP>()));
 }
 
 // vecdot(x, x) of tile row r by the exact recipe (row_sqnorms, distance.py:66-72)
@@ -356,17 +375,17 @@ __device__ __forceinline__ double row_self_sq(const unsigned char* tb, int r, in
 //   acc[to][e] += x[r][e], cnt[to] += 1, sqa[to] += sq, and when from >= 0 the same
 //   amounts are subtracted from cluster `from` (a moved row's signed delta,
 //   engine.py:345-353).  Full passes pass every valid row with from = -1.
-template <int DP>
+// IDENT: row r's values live in lane r (instead of owner_lane(r))
+template <int DP, class TL = TileLayout<DP>, bool IDENT = false>
 __device__ __forceinline__ void accumulate_in_row_order(unsigned rowmask, int to, int from, double sq,
                                                         const unsigned char* tb, double* acc, double* cnt,
                                                         double* sqa, int d, int lane) {
-  using TL = TileLayout<DP>;
   const int e0 = lane < d ? lane : 0;
   const int e1 = lane + 32 < d ? lane + 32 : 0;
   while (rowmask) {
     const int r = __ffs(rowmask) - 1;
     rowmask &= rowmask - 1;
-    const int src = owner_lane(r);
+    const int src = IDENT ? r : owner_lane(r);
     const int t = __shfl_sync(0xffffffffu, to, src);
     const int f = __shfl_sync(0xffffffffu, from, src);
     const double q = __shfl_sync(0xffffffffu, sq, src);

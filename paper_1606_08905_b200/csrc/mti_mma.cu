@@ -353,14 +353,13 @@ struct MtiW12Smem {
 
 template <int DP>
 __global__ void __launch_bounds__(KNB_W12_THREADS, 1) mti_w12_kernel(const MtiArgs a) {
-  using TL = TileLayout<DP>;
+  using TL = TileLayout<DP, 1>;  // written by cp.async only: the fragment-friendly swizzle
   extern __shared__ __align__(1024) unsigned char smem[];
   pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
   if (a.gate && a.ctrl->mti_choice != 0) return;  // the block-dense pass runs this iteration
   const int k = a.k, d = a.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = blockDim.x >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
   const int kp = (k + 7) & ~7, ntile8 = kp >> 3;
   const MtiW12Smem L(DP, k, d, W);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
@@ -395,15 +394,22 @@ __global__ void __launch_bounds__(KNB_W12_THREADS, 1) mti_w12_kernel(const MtiAr
   long long skips = 0, computed = 0, reassigned = 0;
   int qn = 0;
 
-  // async gather of queued entries [0, cnum) into the staging tile: every lane its row
-  auto gather = [&](int cnum) {
+  // async gather of queued entries [0, cnum) into the staging tile: every lane its row.
+  // Returns the row's stored bound (the load stays in flight while the next batch is
+  // filtered): ||x||^2 <= 2 ||c_a||^2 + 2 u^2 bounds the certificate's tolerance, so the
+  // scorer skips its d-term sums.
+  auto gather = [&](int cnum) -> double {
     const uint32_t dst = smem_u32(tb);
+    double uraw = 0.0;
     if (lane < cnum) {
-      const double* src = a.X + (long long)qrow[ring(lane)] * d;
+      const int row = qrow[ring(lane)];
+      const double* src = a.X + (long long)row * d;
 #pragma unroll
       for (int q2 = 0; q2 < DP / 2; ++q2) cp_async16_s(dst + TL::chunk_off(lane, q2, BR), src + 2 * q2);
+      uraw = a.upper[row];  // not yet inflated (the filter leaves survivors' bounds alone)
     }
     cp_async_commit();
+    return uraw;
   };
 
   long long blk = gw;
@@ -455,18 +461,22 @@ __global__ void __launch_bounds__(KNB_W12_THREADS, 1) mti_w12_kernel(const MtiAr
   filter_until(32);
   while (qn > 0) {
     const int cnum = qn < 32 ? qn : 32;
-    gather(cnum);
+    const double uraw = gather(cnum);
     filter_until(32 + cnum);  // the following batch's survivors, overlapping the gather
+    // lane r handles row r from here on (8 consecutive rows per quarter-warp: the exact
+    // tree's row loads hit distinct bank groups)
+    const int r = lane;
+    const bool valid = r < cnum;
+    const int orig = valid ? qorig[ring(r)] : 0;
+    const double xb = valid ? xnorm2_bound(uraw + hd[orig].x, chn[orig]) : 0.0;
     cp_async_wait_all();
     __syncwarp();
-    const Scored sc = score_block<DP, false, true, true>(tb, crow, chn, ntile8, tolk, cmax2, lane);
-    const int r = t4 * 8 + g;
-    const bool valid = r < cnum;
-    int id = sc.id;
-    const double nd = exact_winner_stream<DP>(tb, r, crow, k, sc.flag, id);
-    const int orig = valid ? qorig[ring(r)] : 0;
+    const Scored sc = score_block<DP, false, true, true, true, TL>(tb, crow, chn, ntile8, tolk, cmax2, lane, xb);
+    int id = __shfl_sync(0xffffffffu, sc.id, owner_lane(r));
+    const bool flag = __shfl_sync(0xffffffffu, (int)sc.flag, owner_lane(r)) != 0;
+    const double nd = exact_winner_stream<DP, TL>(tb, r, crow, k, flag, id);
     const bool moved = valid && id != orig;
-    const double sq = moved ? exact_sq_stream<DP, true>(tb, r, nullptr) : 0.0;
+    const double sq = moved ? exact_sq_stream<DP, true, TL>(tb, r, nullptr) : 0.0;
     if (valid) {
       const long long grow = qrow[ring(r)];
       a.upper[grow] = nd;
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(KNB_W12_THREADS, 1) mti_w12_kernel(const MtiAr
       }
     }
     if (lane == 0) computed += (long long)cnum * k;
-    accumulate_in_row_order<DP>(row_mask(moved, r), id, orig, sq, tb, acc, cnt, sqa, d, lane);
+    accumulate_in_row_order<DP, TL, true>(row_mask(moved, r), id, orig, sq, tb, acc, cnt, sqa, d, lane);
     __syncwarp();
     qh = ring(cnum);  // pop the batch
     qn -= cnum;
