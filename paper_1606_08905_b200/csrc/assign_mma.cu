@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
 
   // Per-row state (previous assignment, MTI bound) is prefetched one block ahead so
   // no block starts by waiting on a global load.
-  const int my_r0 = t4 * 8 + g;
+  const int my_r0 = W12 ? lane : t4 * 8 + g;  // W12: lane r handles row r after the scorer
   auto state_row = [&](long long b) -> long long {
     const long long r = b * BR + my_r0;
     return (b < nblk && r < a.n) ? r : 0;
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
       __syncwarp();
     }
     const long long row0 = blk * BR;
-    const int my_r = t4 * 8 + g;  // the row this lane finishes after the quad combine
+    const int my_r = my_r0;  // the row this lane finishes after the scorer
     const bool valid = row0 + my_r < a.n;
     const long long row = row0 + my_r;
     int id = 0;
@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
       skips += (valid && !live) ? 1 : 0;
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
       if (lmask) {
-        const Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
+        Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
+        if constexpr (W12) sc = rows_to_lanes(sc, lane);
         int nid = sc.id;
         double nd, sq = 0.0;
         if constexpr (W12) {
@@ -276,10 +277,12 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
           }
         }
         if (lane == 0) computed += (long long)__popc(lmask) * k;
-        accumulate_in_row_order<DP>(row_mask(live && nid != aa, my_r), nid, aa, sq, tb, acc, cnt, sqa, d, lane);
+        accumulate_in_row_order<DP, TL, W12>(row_mask(live && nid != aa, my_r), nid, aa, sq, tb, acc, cnt, sqa, d,
+                                             lane);
       }
     } else if (!labels) {
-      const Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
+      Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
+      if constexpr (W12) sc = rows_to_lanes(sc, lane);
       id = sc.id;
       double nd2;
       if (sc.flag || a.mti_seed) {
@@ -317,10 +320,11 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
     if (a.mti_filter) {
       // accumulated above
     } else if (!a.delta) {
-      accumulate_in_row_order<DP>(row_mask(valid, my_r), id, -1, my_sq, tb, acc, cnt, sqa, d, lane);
+      accumulate_in_row_order<DP, TL, W12>(row_mask(valid, my_r), id, -1, my_sq, tb, acc, cnt, sqa, d, lane);
     } else {
       // steady-state dense passes: running sums move by the reassigned rows only
-      accumulate_in_row_order<DP>(row_mask(valid && id != old, my_r), id, old, 0.0, tb, acc, cnt, sqa, d, lane);
+      accumulate_in_row_order<DP, TL, W12>(row_mask(valid && id != old, my_r), id, old, 0.0, tb, acc, cnt, sqa, d,
+                                           lane);
     }
     // ---- refill this stage with the block NS strides ahead
     __syncwarp();

@@ -247,6 +247,19 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
   return r;
 }
 
+// Scorer results of row `lane` (score_block leaves row r's in lane owner_lane(r)); after
+// this, lane r handles row r: 8 consecutive rows per quarter-warp, so the exact tree's
+// 16-byte row loads hit 8 distinct bank groups under either tile swizzle
+__device__ __forceinline__ Scored rows_to_lanes(const Scored& sc, int lane) {
+  const int src = owner_lane(lane);
+  Scored o;
+  o.id = __shfl_sync(0xffffffffu, sc.id, src);
+  o.flag = __shfl_sync(0xffffffffu, (int)sc.flag, src) != 0;
+  o.best = __shfl_sync(0xffffffffu, sc.best, src);
+  o.xn2 = __shfl_sync(0xffffffffu, sc.xn2, src);
+  return o;
+}
+
 // Exact recipe on the lane's row: re-rank over every centroid (ascending, strict <,
 // sqrt domain, distance.py:106-116) when flagged, else the distance to `id`.
 template <int DP>
