@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
 
   // Per-row state (previous assignment, MTI bound) is prefetched one block ahead so
   // no block starts by waiting on a global load.
-  const int my_r0 = W12 ? lane : t4 * 8 + g;  // W12: lane r handles row r after the scorer
+  // W12: lane r handles row r after the scorer (rows_to_lanes; measured: the eight-warp
+  // forms do not gain from it -- c3's first pass 1.76 -> 1.83 ms)
+  const int my_r0 = W12 ? lane : t4 * 8 + g;
   auto state_row = [&](long long b) -> long long {
     const long long r = b * BR + my_r0;
     return (b < nblk && r < a.n) ? r : 0;

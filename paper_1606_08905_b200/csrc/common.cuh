@@ -301,7 +301,8 @@ struct Zero {
 // permutation s(r) = 2 (r & 3) + ((r >> 2) & 1) instead of r & 7.  Both spread 8
 // consecutive rows over the 8 bank groups; s also spreads the DMMA A-fragment load
 // (a half-warp reads 4 rows x 2 adjacent chunks: {c ^ s(r)} hits 8 distinct groups,
-// where r & 7 hits 4 twice -- a 2-way conflict on every fragment load)
+// where r & 7 hits 4 twice -- a 2-way conflict on every fragment load).  64-byte rows
+// likewise: s(r) = 2 ((r >> 1) & 1) + ((r >> 2) & 1) instead of (r >> 1) & 3.
 template <int DP, int SW = 0>
 struct TileLayout {
   static constexpr int PW = DP < 16 ? DP : 16;      // doubles per panel row
@@ -311,6 +312,7 @@ struct TileLayout {
   __device__ static __forceinline__ int swz(int r) {
     if constexpr (RB == 128 && SW == 1) return ((r & 3) << 1) | ((r >> 2) & 1);
     else if constexpr (RB == 128) return r & 7;
+    else if constexpr (RB == 64 && SW == 1) return (((r >> 1) & 1) << 1) | ((r >> 2) & 1);
     else if constexpr (RB == 64) return (r >> 1) & 3;
     else if constexpr (RB == 32) return (r >> 2) & 1;
     else return 0;

@@ -262,10 +262,9 @@ __device__ __forceinline__ Scored rows_to_lanes(const Scored& sc, int lane) {
 
 // Exact recipe on the lane's row: re-rank over every centroid (ascending, strict <,
 // sqrt domain, distance.py:106-116) when flagged, else the distance to `id`.
-template <int DP>
+template <int DP, class TL = TileLayout<DP>>
 __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, const double* crow, int k, int d,
                                                bool flag, int& id, double* sq_out) {
-  using TL = TileLayout<DP>;
   double x[DP];
 #pragma unroll
   for (int q2 = 0; q2 < DP / 2; ++q2) {
@@ -370,9 +369,8 @@ __device__ __forceinline__ double exact_winner_stream(const unsigned char* tb, i
 }
 
 // vecdot(x, x) of tile row r by the exact recipe (row_sqnorms, distance.py:66-72)
-template <int DP>
+template <int DP, class TL = TileLayout<DP>>
 __device__ __forceinline__ double row_self_sq(const unsigned char* tb, int r, int d) {
-  using TL = TileLayout<DP>;
   double x[DP];
 #pragma unroll
   for (int q2 = 0; q2 < DP / 2; ++q2) {

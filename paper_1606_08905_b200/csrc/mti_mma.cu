@@ -71,7 +71,7 @@ struct MtiMmaSmem {
 template <int DP, bool HOST, bool SMALLK, bool LEAN>
 __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1)
     mti_mma_kernel(const MtiArgs a) {
-  using TL = TileLayout<DP>;
+  using TL = TileLayout<DP, 1>;  // tiles written by cp.async only: the fragment-friendly swizzle
   constexpr int KS = DP / 4;
   extern __shared__ __align__(1024) unsigned char smem[];
   pdl_enter();
@@ -172,15 +172,16 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
 
   // score and update the first `cnum` queued survivors (cnum <= 32), staged in tb
   auto process = [&](const unsigned char* tb, int cnum) {
-    const Scored sc = score_block<DP, SMALLK, LEAN>(tb, bf, chn, ntile8, tolk, cmax2, lane);
-    const int r = t4 * 8 + g;
+    const Scored sc = rows_to_lanes(score_block<DP, SMALLK, LEAN, false, false, TL>(tb, bf, chn, ntile8, tolk,
+                                                                                     cmax2, lane), lane);
+    const int r = lane;  // lane r handles row r from here on
     const bool valid = r < cnum;
     int id = sc.id;
-    const double nd = exact_winner<DP>(tb, r, crow, k, d, sc.flag, id, nullptr);
+    const double nd = exact_winner<DP, TL>(tb, r, crow, k, d, sc.flag, id, nullptr);
     const int orig = valid ? qorig[ring(r)] : 0;
     const bool moved = valid && id != orig;
     // ||x||^2 only for the (few) moved rows whose signed deltas carry it
-    const double sq = moved ? row_self_sq<DP>(tb, r, d) : 0.0;
+    const double sq = moved ? row_self_sq<DP, TL>(tb, r, d) : 0.0;
     if (valid) {
       const long long grow = qrow[ring(r)];
       a.upper[grow] = nd;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
       }
     }
     if (lane == 0) computed += (long long)cnum * k;
-    accumulate_in_row_order<DP>(row_mask(moved, r), id, orig, sq, tb, acc, cnt, sqa, d, lane);
+    accumulate_in_row_order<DP, TL, true>(row_mask(moved, r), id, orig, sq, tb, acc, cnt, sqa, d, lane);
     __syncwarp();
   };
 
