@@ -42,8 +42,8 @@ struct MtiMmaSmem {
     bf = o;    o += (size_t)kp * DP * 8;
     crow = o;  o += (size_t)kp * (DP + 2) * 8;
     chn = o;   o += (size_t)kp * 8;
-    hmin = o;  o += (size_t)k * 8;
-    drift = o; o += (size_t)k * 8;
+    hmin = o;  o += (size_t)k * 16;  // {drift, half_min} pairs
+    drift = hmin;
     red = o;   o += 16 * 8 * 8;
     o = al(o, 1024);
     warp0 = o;
@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
   double* bf = reinterpret_cast<double*>(smem + L.bf);
   double* crow = reinterpret_cast<double*>(smem + L.crow);
   double* chn = reinterpret_cast<double*>(smem + L.chn);
-  double* hmin = reinterpret_cast<double*>(smem + L.hmin);
-  double* drift = reinterpret_cast<double*>(smem + L.drift);
+  double2* hd = reinterpret_cast<double2*>(smem + L.hmin);  // {drift, half_min} per centroid
   double* red = reinterpret_cast<double*>(smem + L.red);
   unsigned char* wbase = smem + L.warp0 + (size_t)warp * L.per_warp;
   unsigned char* tb = wbase + L.tile_off;
@@ -109,10 +108,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
     bf[i] = (jb < k && eb < d) ? a.means[(long long)jb * d + eb] : 0.0;
   }
   for (int j = tid; j < kp; j += blockDim.x) chn[j] = j < k ? a.chn[j] : -CUDART_INF;
-  for (int j = tid; j < k; j += blockDim.x) {
-    hmin[j] = a.half_min[j];
-    drift[j] = a.drift[j];
-  }
+  for (int j = tid; j < k; j += blockDim.x) hd[j] = make_double2(a.drift[j], a.half_min[j]);
   for (int i = lane; i < k * d; i += 32) acc[i] = 0.0;
   for (int j = lane; j < k; j += 32) { cnt[j] = 0.0; sqa[j] = 0.0; }
   __syncthreads();
@@ -122,7 +118,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
   const long long nblk = (a.n + BR - 1) / BR;
   const long long gw = (long long)blockIdx.x * W + warp, TW = (long long)gridDim.x * W;
   const bool vec = ((d & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
-  long long skips = 0, computed = 0, reassigned = 0;
+  long long computed = 0, reassigned = 0;
   int qn = 0;
   // both staging tiles start zeroed: padded dims stay zero, rows past a batch hold stale finite data
   for (int i = lane; i < 2 * BR * DP; i += 32) reinterpret_cast<double*>(tb)[i] = 0.0;
@@ -198,26 +194,33 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
 
   // filter strided blocks (bound inflation + clause 1) until `target` survivors are queued.
   // The per-row state of the NEXT group of FB blocks is loaded while the current group is
-  // filtered (and across calls), so the loads' latency overlaps useful work.
-  long long blk = gw;
+  // filtered (and across calls), so the loads' latency overlaps useful work.  Row and
+  // block indices are 32-bit (the launcher only runs shards below 2^31 - 2^26 rows).
+  const int n32 = (int)a.n, nblk32 = (n32 + BR - 1) / BR, TW32 = (int)TW;
+  int blk = (int)gw;
+  const int32_t* __restrict__ g_assign = a.assign;
+  double* __restrict__ g_upper = a.upper;
+  uint8_t* __restrict__ g_tight = a.tight;
   constexpr int FB = DP <= 32 ? 4 : 2;  // (DP = 64 is register-bound)
   // (measured: prefetching at DP = 32 costs 1.6% at c2 -- the registers matter more)
   constexpr bool PREFETCH = DP <= 16;
   int pa[FB], ps[FB];
   double pu[FB];
-  auto load_group = [&](long long b) {
+  auto load_group = [&](int b) {
 #pragma unroll
     for (int j = 0; j < FB; ++j) {
-      const long long row = (b + j * TW) * BR + lane;
-      const bool ok = b + j * TW < nblk && row < a.n;
-      pa[j] = ok ? a.assign[row] : -1;
-      pu[j] = ok ? a.upper[row] : 0.0;
+      const int bj = b + j * TW32;
+      const int row = bj * BR + lane;
+      const bool ok = bj < nblk32 && row < n32;
+      pa[j] = ok ? g_assign[row] : -1;
+      pu[j] = ok ? g_upper[row] : 0.0;
       if constexpr (HOST) ps[j] = (ok && cslot) ? cslot[row] : -1;
     }
   };
   if constexpr (PREFETCH) load_group(blk);
+  int skips32 = 0;
   auto filter_until = [&](int target) {
-    while (qn < target && blk < nblk) {
+    while (qn < target && blk < nblk32) {
       if constexpr (!PREFETCH) load_group(blk);
       int aa[FB], sl[FB];
       double uu[FB];
@@ -227,32 +230,29 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
         uu[j] = pu[j];
         if constexpr (HOST) sl[j] = ps[j];
       }
-      const long long cur = blk;
-      blk += FB * TW;
+      const int cur = blk;
+      blk += FB * TW32;
       if constexpr (PREFETCH) load_group(blk);  // prefetch the next group
 #pragma unroll
       for (int j = 0; j < FB; ++j) {
-        if (cur + j * TW >= nblk) break;  // uniform
-        const long long row = (cur + j * TW) * BR + lane;
-        bool live = false;
-        if (aa[j] >= 0) {
-          double u = uu[j];
-          const double dr = drift[aa[j]];
-          u = u + dr;  // u + 0.0 == u
-          if (u <= hmin[aa[j]]) {
-            ++skips;
-            if (dr != 0.0) {  // the inflated bound is the skipped row's final state
-              a.upper[row] = u;
-              a.tight[row] = 0;
-            }
-          } else {
-            live = true;  // a survivor's bound and tight flag are rewritten by its scan
-          }
+        const int bj = cur + j * TW32;
+        if (bj >= nblk32) break;  // uniform
+        const int row = bj * BR + lane;
+        const int aj = aa[j] < 0 ? 0 : aa[j];
+        const double2 dh = hd[aj];  // {drift, half_min}
+        const double u = uu[j] + dh.x;  // u + 0.0 == u
+        const bool valid = aa[j] >= 0;
+        const bool skip = valid && u <= dh.y;
+        const bool live = valid && !skip;  // a survivor's bound and tight flag are rewritten by its scan
+        skips32 += skip;
+        if (skip && dh.x != 0.0) {  // the inflated bound is the skipped row's final state
+          g_upper[row] = u;
+          g_tight[row] = 0;
         }
         const unsigned b = __ballot_sync(0xffffffffu, live);
         if (live) {
           const int pos = ring(qn + __popc(b & ((1u << lane) - 1u)));
-          qrow[pos] = (int)row;
+          qrow[pos] = row;
           qorig[pos] = aa[j];
           if (HOST && cslot) qsrc[pos] = sl[j];
         }
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
     for (int w = 0; w < W; ++w) v += reinterpret_cast<const double*>(smem + L.warp0 + (size_t)w * L.per_warp + off)[ii];
     out[i] = v;
   }
-  const long long v0 = warp_sum_ll(reassigned), v1 = warp_sum_ll(computed), v2 = warp_sum_ll(skips);
+  const long long v0 = warp_sum_ll(reassigned), v1 = warp_sum_ll(computed), v2 = warp_sum_ll((long long)skips32);
   if (lane == 0) { red[warp * 8 + 0] = (double)v0; red[warp * 8 + 1] = (double)v1; red[warp * 8 + 2] = (double)v2; }
   __syncthreads();
   if (tid == 0) {
