@@ -122,7 +122,8 @@ __device__ __forceinline__ void load_block(const CUtensorMap* tmap, uint64_t* ba
 #ifndef KNB_DENSE_W12_THREADS
 #define KNB_DENSE_W12_THREADS 384
 #endif
-template <int DP, bool SMALLK, bool W12 = false>
+// ONE (k <= 8): the scorer's single-tile form (half the DMMAs of a padded tile pair)
+template <int DP, bool SMALLK, bool W12 = false, bool ONE = false>
 __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 2 : 1)
     dense_mma_kernel(const __grid_constant__ CUtensorMap tmap, const DenseArgs a) {
   using TL = TileLayout<DP>;
@@ -259,7 +260,8 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
       skips += (valid && !live) ? 1 : 0;
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
       if (lmask) {
-        Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
+        Scored sc = score_block<DP, SMALLK, W12, W12, false, TL, ONE>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2,
+                                                                     lane);
         if constexpr (W12) sc = rows_to_lanes(sc, lane);
         int nid = sc.id;
         double nd, sq = 0.0;
@@ -283,7 +285,8 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
                                              lane);
       }
     } else if (!labels) {
-      Scored sc = score_block<DP, SMALLK, W12, W12>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2, lane);
+      Scored sc = score_block<DP, SMALLK, W12, W12, false, TL, ONE>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2,
+                                                                   lane);
       if constexpr (W12) sc = rows_to_lanes(sc, lane);
       id = sc.id;
       double nd2;
@@ -401,21 +404,22 @@ bool use_w12(int DP, int k, int d) {
   return env && d == DP && (DP == 16 || DP == 32) && k > 16 && warps_for(DP, k, d, true) >= 12;
 }
 
-template <int DP, bool SMALLK, bool W12 = false>
+template <int DP, bool SMALLK, bool W12 = false, bool ONE = false>
 cudaError_t launch_mma_k(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
   const int W = warps_for(DP, a.k, a.d, W12);
   if (!W) return cudaErrorInvalidValue;
   const WarpSmem L(DP, a.k, a.d, W, W12);
-  cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<DP, SMALLK, W12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)L.total);
+  cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<DP, SMALLK, W12, ONE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  return launch_pdl(dense_mma_kernel<DP, SMALLK, W12>, dim3(grid), dim3(W * 32), L.total, s, *tmap, a);
+  return launch_pdl(dense_mma_kernel<DP, SMALLK, W12, ONE>, dim3(grid), dim3(W * 32), L.total, s, *tmap, a);
 }
 
 template <int DP>
 cudaError_t launch_mma_dp(const CUtensorMap* tmap, const DenseArgs& a, int grid, cudaStream_t s) {
   if constexpr (DP == 16 || DP == 32)
     if (use_w12(DP, a.k, a.d)) return launch_mma_k<DP, false, true>(tmap, a, grid, s);
+  if (a.k <= 8) return launch_mma_k<DP, true, false, true>(tmap, a, grid, s);  // c1: 0.0248 -> 0.0228 ms / iter
   return a.k <= 16 ? launch_mma_k<DP, true>(tmap, a, grid, s) : launch_mma_k<DP, false>(tmap, a, grid, s);
 }
 

@@ -11,6 +11,7 @@
 #define KNB_EXPERIMENT 0
 #endif
 
+
 namespace knb {
 
 constexpr int BR = 32;  // rows per warp block
@@ -115,8 +116,9 @@ struct Scored {
 // XB: the caller knows an upper bound of ||x||^2 for every row (lane r holds row r's in
 // xb); the certificate only needs an upper bound, so the d-term sums are skipped.
 // TL: the staging tile's layout (TileLayout<DP> or its cp.async-only variant)
+// ONE: k <= 8 (a single centroid tile; the dense pass instantiates it for such k)
 template <int DP, bool SMALLK = false, bool LEAN = false, bool BCROW = false, bool XB = false,
-          class TL = TileLayout<DP>>
+          class TL = TileLayout<DP>, bool ONE = false>
 __device__ __forceinline__ Scored score_block(const unsigned char* tb, const double* bf, const double* chn,
                                               int ntile8, double tolk, double cmax2, int lane, double xb = 0.0) {
   constexpr int KS = DP / 4;
@@ -212,9 +214,32 @@ __device__ __forceinline__ Scored score_block(const unsigned char* tb, const dou
       merge_later(best[pg], bid[pg], flag[pg], pb, pi, pf, tolhi[pg]);
     }
   };
+  // k <= 8 (one tile): only the real tile's DMMAs; the second set stays at -inf
+  auto mma_one = [&](double (&c0)[4][2], double (&c1)[4][2]) {
+    const double2 h0 = *reinterpret_cast<const double2*>(chn + 2 * t4);
+#pragma unroll
+    for (int pg = 0; pg < 4; ++pg) {
+      c0[pg][0] = h0.x; c0[pg][1] = h0.y;
+      c1[pg][0] = -CUDART_INF; c1[pg][1] = -CUDART_INF;
+    }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double bv0;
+      if constexpr (BCROW) bv0 = bf[g * crow_stride<DP>() + ks * 4 + t4];
+      else bv0 = bf[(ks << 5) + lane];
+#pragma unroll
+      for (int pg = 0; pg < 4; ++pg) {
+        double av;
+        if constexpr (ACACHE) av = afr[pg][ks];
+        else av = *reinterpret_cast<const double*>(tb + TL::elem_off(pg * 8 + g, ks * 4 + t4, BR));
+        dmma(c0[pg], av, bv0);
+      }
+    }
+  };
   double ca0[4][2], ca1[4][2];
-  mma_step(0, ca0, ca1);
-  if constexpr (SMALLK) {
+  if constexpr (ONE) mma_one(ca0, ca1);
+  else mma_step(0, ca0, ca1);
+  if constexpr (SMALLK || ONE) {
     epilogue(0, ca0, ca1);
   } else if constexpr (LEAN) {
     epilogue(0, ca0, ca1);
