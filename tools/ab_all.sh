@@ -1,4 +1,4 @@
-for i in 1 2; do for lib in variants/h4.so ""; do
+for i in 1 2; do for lib in variants/h5.so ""; do
 for c in c3 c1; do
 KNB_LIB=$lib timeout 600 python bench.py --config $c --no-e2e --no-cpu --steps 40 2>/dev/null | python -c "
 import json,sys; l=json.loads(sys.stdin.read().strip().splitlines()[-1])
