@@ -60,6 +60,11 @@ CASES = {
                      cfg=dict(k=10, init="kmeanspp", seed=36, pruning=True, max_iters=20)),
     "k50_pruned": dict(data=lambda: mixture(MixtureSpec(20000, 8, 50, 37, "uniform", -3, 3, 0.5, 1.0)),
                        cfg=dict(k=50, seed=37, pruning=True, max_iters=25)),
+    # d == DP in {16, 32} with k > 16: the twelve-warp MTI and dense kernels
+    "d16_k24_pruned": dict(data=lambda: mixture(MixtureSpec(6000, 16, 24, 38, "uniform", -4, 4, 1.0)),
+                           cfg=dict(k=24, seed=38, pruning=True, max_iters=30)),
+    "d32_k24_dense": dict(data=lambda: mixture(MixtureSpec(4000, 32, 24, 39, "uniform", -3, 3, 1.0)),
+                          cfg=dict(k=24, seed=39, pruning=False, max_iters=25)),
     # BASELINE configs: config 1 in full, the others at reduced n with the same laws
     "c1_full": dict(data=lambda: mixture(MixtureSpec(200_000, 16, 8, 1, "uniform", -10, 10, 1.0)),
                     cfg=dict(k=8, init="forgy", seed=1, pruning=False, max_iters=20, tolerance=0)),
