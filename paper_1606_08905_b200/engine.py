@@ -310,6 +310,7 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         stream = torch_stream(device)  # NCCL orders its all-reduce after torch's current stream
     cls = context_cls or _native.Context
     ctx = cls(device, n, n_local, row_lo, d, k, cfg.pruning, cfg.max_iters, cfg.tolerance, stream)
+    out_pool = None
     try:
         _apply_options(ctx, cfg)
         inspect_cache = False
@@ -330,7 +331,6 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         history = [] if cfg.collect_assignments else None
         walls: list[float] = []
         batched = comm.world == 1 and history is None and not cfg.validate_bounds
-        out_pool = None
         if batched:
             t0 = time.perf_counter()
             out_pool, out_buf = _prefetch_output(n_local)
@@ -387,7 +387,6 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         row_cache = ctx.sem_cache() if inspect_cache else None
         if out_pool is not None:
             assignments = ctx.assignments(out=out_buf.result())
-            out_pool.shutdown()
         else:
             assignments = ctx.assignments()
         peak = ctx.state_bytes()
@@ -404,6 +403,8 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
             row_cache=row_cache,
         )
     finally:
+        if out_pool is not None:
+            out_pool.shutdown(wait=False)
         ctx.close()
 
 
