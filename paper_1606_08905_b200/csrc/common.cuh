@@ -268,6 +268,38 @@ __device__ __forceinline__ double warp_exact_sq(const TX* __restrict__ x, const 
   return dot;
 }
 
+// vecdot(x, x) by a whole warp, bit-identical to exact_self_rt (warp_exact_sq's tree
+// with x - 0 == x)
+__device__ __forceinline__ double warp_exact_self(const double* __restrict__ x, int d, int lane) {
+  const int n1 = d & ~15, n32 = n1 & ~31;
+  double dot = 0.0;
+  if (n1) {
+    double z = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < n32; i += 32) {
+      const double v = x[i + lane];
+      z = __fma_rn(v, v, z);
+    }
+    const int a = lane >> 3, l = lane & 7;
+    double acc = __dadd_rn(z, __shfl_down_sync(0xffffffffu, z, 4));
+    for (int i = n32; i < n1; i += 16) {
+      if (l < 4) {
+        const double v = x[i + 4 * a + l];
+        acc = __fma_rn(v, v, acc);
+      }
+    }
+    const double a1 = __shfl_down_sync(0xffffffffu, acc, 8);
+    const double a2 = __shfl_down_sync(0xffffffffu, acc, 16);
+    const double a3 = __shfl_down_sync(0xffffffffu, acc, 24);
+    const double sl = __dadd_rn(__dadd_rn(__dadd_rn(acc, a1), a2), a3);
+    const double s0 = __shfl_sync(0xffffffffu, sl, 0), s1 = __shfl_sync(0xffffffffu, sl, 1);
+    const double s2 = __shfl_sync(0xffffffffu, sl, 2), s3 = __shfl_sync(0xffffffffu, sl, 3);
+    dot = __dadd_rn(__dadd_rn(s0, s2), __dadd_rn(s1, s3));
+  }
+  for (int i = n1; i < d; ++i) dot = __fma_rn(x[i], x[i], dot);
+  return dot;
+}
+
 // The tail of warp_exact_sq for d a multiple of 32 (no 16-wide or scalar blocks):
 // lane 8a + l holds z[a][l]; returns the tree's dot in every lane.
 __device__ __forceinline__ double warp_tree_finish(double z, int lane) {

@@ -25,6 +25,8 @@ namespace knb {
 
 namespace {
 
+constexpr int GEO_PAIRS_MAX_K = 256;  // beyond: one warp per row (k^2 warps would be many)
+
 // LPE lanes per element: lane q sums CTA partials [q*S, (q+1)*S) in CTA order
 // (S = ceil(G/LPE), loads batched 16 deep), then the LPE sums combine in a fixed
 // butterfly -- a fixed order for a given (G, L), so runs are bit-reproducible.  Short
@@ -130,10 +132,18 @@ __device__ void finalize_centroid(const FinalArgs& f, int j) {
     if (occ) m[e] = sums[e] / cntj;
   }
   __syncwarp();
+  // drift and ||c||^2 by the whole warp (the same trees as exact_sq_rt / exact_self_rt)
+  const double dsq = warp_exact_sq(m, pv, d, lane);
+  const double n2 = warp_exact_self(m, d, lane);
+  if (f.pruning && k <= GEO_PAIRS_MAX_K) {  // the pair-wise geometry fills in the rest
+    if (lane == 0) {
+      f.half_min[j] = CUDART_INF;
+      f.half[(long long)j * k + j] = 0.0;
+    }
+  }
   if (lane == 0) {
-    f.drift[j] = occ ? sqrt(exact_sq_rt(m, pv, d)) : 0.0;
+    f.drift[j] = occ ? sqrt(dsq) : 0.0;
     f.counts[j] = cntj;
-    const double n2 = exact_self_rt(m, d);
     f.cn2[j] = n2;
     f.chn[j] = -0.5 * n2;
     if (f.wcss_mode == 1) {  // sq - ||sums||^2 / count, clamped at 0 (engine.py:385-388)
@@ -220,6 +230,30 @@ __device__ void geometry_row(const FinalArgs& f, int a) {
   if (lane == 0) f.half_min[a] = mn;  // +inf when k == 1
 }
 
+// k <= GEO_PAIRS_MAX_K: one warp per centroid pair a < b (warp-wide exact tree), the
+// row minima by atomicMin on the bit patterns (non-negative doubles order like their
+// bits; min is order-free, so the result is deterministic).  finalize reset half_min
+// to +inf and the diagonal to 0.
+__global__ void geometry_pairs_kernel(const FinalArgs f) {
+  pdl_enter();
+  const Ctrl* c = f.ctrl;
+  if (c->stop && !c->ignore_stop) return;
+  const int k = f.k, d = f.d, lane = threadIdx.x & 31;
+  const long long p = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (p >= (long long)k * k) return;
+  const int a = (int)(p / k), b = (int)(p - (long long)a * k);
+  if (b <= a) return;  // warp-uniform
+  // rowwise_distances(means[a+1:], means[a]) * 0.5: x = means[b], c = means[a]
+  const double h = sqrt(warp_exact_sq(f.means + (long long)b * d, f.means + (long long)a * d, d, lane)) * 0.5;
+  if (lane == 0) {
+    f.half[(long long)a * k + b] = h;
+    f.half[(long long)b * k + a] = h;
+    const unsigned long long hb = (unsigned long long)__double_as_longlong(h);
+    atomicMin(reinterpret_cast<unsigned long long*>(f.half_min + a), hb);
+    atomicMin(reinterpret_cast<unsigned long long*>(f.half_min + b), hb);
+  }
+}
+
 __global__ void geometry_kernel(const FinalArgs f) {
   pdl_enter();
   const Ctrl* c = f.ctrl;
@@ -302,6 +336,10 @@ cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t s) {
 }
 
 cudaError_t launch_geometry(const FinalArgs& f, cudaStream_t s) {
+  if (f.k <= GEO_PAIRS_MAX_K) {
+    const long long warps = (long long)f.k * f.k;
+    return launch_pdl(geometry_pairs_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, s, f);
+  }
   const int wpb = 8;
   return launch_pdl(geometry_kernel, dim3((f.k + wpb - 1) / wpb), dim3(wpb * 32), 0, s, f);
 }
