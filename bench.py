@@ -144,11 +144,23 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
-def workload(name: str, n: int | None):
+# Multi-GPU series: c3 / c4 / c5 are the BASELINE configs "row-sharded over 1/2/4/8 GPUs"
+# (total n fixed: strong scaling).  c1 / c2 are a few hundred microseconds per iteration on
+# ONE GPU; split 8 ways the per-GPU pass would be latency-bound and the all-reduce would
+# dominate, so their series keeps n rows PER GPU (weak scaling: total n = n x N).
+WEAK = ("c1", "c2")
+
+
+def workload(name: str, n: int | None, world: int = 1):
     from paper_1606_08905_b200 import synth
     cfg = dict(synth.CONFIGS[name])
-    n = n or cfg["n"]
+    if n is None:
+        n = cfg["n"] * (world if name in WEAK else 1)
     return cfg, n
+
+
+def scaling_of(name: str, n_given) -> str:
+    return "weak" if (name in WEAK and n_given is None) else "strong"
 
 
 def cpu_port_run(name, cfg, n_sub, iters, threads):
@@ -178,13 +190,13 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg, n = workload(args.config, args.n)
+    cfg, n = workload(args.config, args.n, int(os.environ.get("WORLD_SIZE", "1")))
     base = cpu_baseline(args.config, cfg, args.warmup, args.steps)
     n_sub = min(CPU_SAMPLE[args.config], cfg["n"])
     line = {
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * n_sub / base["value"], "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": scaling_of(args.config, args.n), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "n": n, "n_sample": n_sub, "k": cfg["k"], "init": cfg["init"],
                    "pruning": cfg["pruning"]},
         "impl": "reference", "cpu_baseline": base,
@@ -212,7 +224,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         comm = TorchComm()
     name = args.config
-    cfg, n = workload(name, args.n)
+    cfg, n = workload(name, args.n, world)
     k = cfg["k"]
     seed = int(name[1:])
     t_gen = time.perf_counter()
@@ -426,10 +438,12 @@ def run_ours(args):
     launches_per_step = 12 if tc else 4 + (1 if cfg["pruning"] else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": scaling_of(name, args.n),
         "vs_baseline": None, "dtype": "f32 rows: tf32 tensor-core scores + f64 certificate/rerank/sums" if tc else "f64",
         "data": "synthetic",
-        "config": {"workload": name, "n": n, "d": d, "k": k, "init": cfg["init"], "pruning": cfg["pruning"],
+        "config": {"workload": name, "n": n, "n_per_gpu": hi - lo, "d": d, "k": k, "init": cfg["init"],
+                   "pruning": cfg["pruning"],
                    "tolerance": cfg["tolerance"], "parallelism": f"row-shard x{world}",
                    "l2": f"inputs {shard_bytes / 2**20:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
                    if shard_bytes > 126e6 else "inputs smaller than L2 (launch-bound config)",
