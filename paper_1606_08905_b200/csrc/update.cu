@@ -132,18 +132,15 @@ __device__ void finalize_centroid(const FinalArgs& f, int j) {
     if (occ) m[e] = sums[e] / cntj;
   }
   __syncwarp();
-  // drift and ||c||^2 by the whole warp (the same trees as exact_sq_rt / exact_self_rt)
-  const double dsq = warp_exact_sq(m, pv, d, lane);
-  const double n2 = warp_exact_self(m, d, lane);
-  if (f.pruning && k <= GEO_PAIRS_MAX_K) {  // the pair-wise geometry fills in the rest
-    if (lane == 0) {
+  // (lane 0's sequential trees: measured faster here than warp_exact_sq's shuffle chain)
+  if (lane == 0) {
+    if (f.pruning && k <= GEO_PAIRS_MAX_K) {  // the pair-wise geometry fills in the rest
       f.half_min[j] = CUDART_INF;
       f.half[(long long)j * k + j] = 0.0;
     }
-  }
-  if (lane == 0) {
-    f.drift[j] = occ ? sqrt(dsq) : 0.0;
+    f.drift[j] = occ ? sqrt(exact_sq_rt(m, pv, d)) : 0.0;
     f.counts[j] = cntj;
+    const double n2 = exact_self_rt(m, d);
     f.cn2[j] = n2;
     f.chn[j] = -0.5 * n2;
     if (f.wcss_mode == 1) {  // sq - ||sums||^2 / count, clamped at 0 (engine.py:385-388)
