@@ -19,6 +19,9 @@
 // queued gathers their rows from HBM into a swizzled 32-row tile and scores them with
 // score_block (mma_common.cuh).  Deltas go through the warp-local row-ordered walk
 // into warp-private sums; the CTA adds its warps' sums in warp order.
+// Two forms: mti_mma_kernel (eight warps, two staging tiles per warp; k <= 16, rows in
+// host memory, other shapes) and mti_w12_kernel (twelve warps per SM, one staging tile
+// each; d == DP in {16, 32} with k > 16 -- config 2).
 #include <cuda.h>
 #include <math_constants.h>
 
@@ -599,7 +602,9 @@ cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
   if constexpr (DP == 16 || DP == 32) {
     // (KNB_MTI_W12=0: the two-tile eight-warp kernel, for A/B measurements)
     static const int w12_env = [] { const char* v = getenv("KNB_MTI_W12"); return v ? atoi(v) : 1; }();
-    if (w12_env && a.k > 16 && w12_warps_for(DP, a.k, a.d)) return launch_w12<DP>(a, grid, s);
+    // (16-byte cp.async row copies: rows must be 16-byte aligned, e.g. not a view at an odd offset)
+    if (w12_env && a.k > 16 && w12_warps_for(DP, a.k, a.d) && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0)
+      return launch_w12<DP>(a, grid, s);
   }
   if (a.k <= 16) return launch_host<DP, false, true>(a, grid, s);
   if constexpr (DP == 32) return launch_host<DP, false, false, true>(a, grid, s);
