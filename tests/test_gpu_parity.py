@@ -144,6 +144,23 @@ def test_torch_device_input_is_used_in_place():
     assert np.array_equal(a.centroids.means, b.centroids.means)
 
 
+def test_misaligned_device_view_matches_reference_golden():
+    """A CUDA tensor at an 8-byte (not 16-byte) offset: the twelve-warp MTI form needs
+    16-byte rows, so the eight-warp form takes over -- same reference results."""
+    import torch
+    m = case_data("d16_k24_pruned")
+    flat = torch.empty(m.size + 1, dtype=torch.float64, device="cuda")
+    view = flat[1:].view(m.shape)
+    view.copy_(torch.from_numpy(m))
+    assert view.data_ptr() % 16 == 8
+    r = kb.kmeans(view, _cfg("d16_k24_pruned", collect_assignments=True))
+    g = golden("d16_k24_pruned")
+    assert r.n_iterations == len(g["reassignments"])
+    assert np.array_equal(r.assignments, g["assignments"].astype(np.int32))
+    assert np.array_equal([s.skips for s in r.iterations], g["skips"])
+    np.testing.assert_allclose(r.centroids.means, g["means"], rtol=0, atol=1e-9 * np.abs(g["means"]).max())
+
+
 def test_nonfinite_rejected_on_device():
     m = kb.synth.uniform(5000, 4, 1)
     m[3210, 2] = np.inf
