@@ -8,7 +8,9 @@ mixture of 32 Gaussians, kmeans++ init, MTI pruning on.  W warm-up iterations
 run first (iteration 0 is the dense full pass), then exactly K iterations are
 timed with CUDA events on the launching stream, bracketed by barrier +
 synchronize, max over ranks.  The run keeps iterating after convergence (every
-timed step does the work of a real iteration of that run).
+timed step does the work of a real iteration of that run).  Under torchrun
+(--gpus N) the rows are sharded over the ranks: c3 / c4 / c5 keep the BASELINE
+total n (strong scaling); c1 / c2 keep n rows per GPU (weak scaling, see WEAK).
 
 Other keys: roofline (the step's dominant kernel, north-star definition:
 dense-equivalent n*k*d FMAs vs point bytes), roofline_k1 (the dense assign
