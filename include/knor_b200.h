@@ -199,13 +199,27 @@ int knb_set_stream(knb_ctx* ctx, void* stream);
 #define KNB_MTI_EXACT 1
 #define KNB_MTI_DENSE 2
 #define KNB_MTI_BLOCK 3
+/* KNB_MTI_TC: the block pass on the tcgen05 tensor cores for f64 rows with d == 16 and
+ * k <= 128 (split-TF32 scores, certified argmin, exact re-rank of uncertified rows; same
+ * outputs as BLOCK).  Under KNB_MTI_AUTO it replaces BLOCK wherever it applies. */
+#define KNB_MTI_TC 4
 int knb_set_option(knb_ctx* ctx, int32_t option, int64_t value);
+/* 1 when a shard of n_local rows may run the compacted (DENSE) MTI kernel, whose filter
+ * uses 32-bit row indices (n_local <= 2^31 - 2^26); larger shards run the BLOCK pass under
+ * KNB_MTI_AUTO / KNB_MTI_DENSE (same results).  Host-only, no device needed. */
+int knb_mti_compact_ok(int64_t n_local);
 /* Device bytes held by the context (the GPU analogue of KmeansResult.peak_state_bytes). */
 int knb_state_bytes(knb_ctx* ctx, int64_t* bytes);
 /* Which kernels the context uses: padded width (0 = generic, < 0: f32 rows on the tcgen05
  * path with that padded width), TMA on/off, grid sizes (grid_mti < 0: the tensor-core MTI
  * kernel with -grid_mti CTAs). */
 int knb_describe(knb_ctx* ctx, int32_t* dense_dp, int32_t* use_tma, int32_t* grid_dense, int32_t* grid_mti);
+/* The tcgen05 MTI pass (KNB_MTI_TC): whether it applies to this context, and how many
+ * rows it could not certify (re-ranked with the exact recipe) since the run started. */
+int knb_mti_tc_info(knb_ctx* ctx, int32_t* available, int64_t* uncertified);
+/* Test hook: the pass's split-TF32 scores D~ (n_local x N floats, N = k rounded up to 16,
+ * ~ ||x - c_j||^2) against the current centroids, into device memory; no state changes. */
+int knb_mti_tc_scores(knb_ctx* ctx, float* dev_out);
 
 /* numpy's default_rng(seed).random(...) on the device: writes draws [first_draw,
  * first_draw + count) of the PCG64 stream whose (state, inc) the host read from

@@ -27,6 +27,31 @@ def _tie():
     return np.array([[0.0, 0.0], [0.0, 1.0], [0.0, -1.0], [0.0, 2.0], [0.0, 0.5]])
 
 
+def _tie_pruned(copies: int = 1, d: int = 2):
+    """Exact ties between a survivor's CURRENT centroid and a lower id in a pruned pass.
+
+    Per copy: clusters {(-2,0), (-1,0), (-1,2)} and {(1,0), (3,0), (0,2)} (given centroids
+    (-1.5, 0.5) and (1, 1.5)); after the first update the means are (-4/3, 2/3) and
+    (4/3, 2/3), so (0, 2) -- assigned to the higher id -- is exactly equidistant from both
+    and off their segment: it survives clause 1 and clause 2 (u > half_dist), and
+    scan_block keeps it (pruning.py:199: switch only on dx < u), while an exhaustive
+    lowest-id argmin would move it.  Copies sit 1000 apart on their own axis (dims >= 2)."""
+    base = np.array([[-2.0, 0.0], [-1.0, 0.0], [-1.0, 2.0], [1.0, 0.0], [3.0, 0.0], [0.0, 2.0]])
+    init = np.array([[-1.5, 0.5], [1.0, 1.5]])
+    rows, cents = [], []
+    for i in range(copies):
+        off = np.zeros(d)
+        if copies > 1:
+            off[2 + i % (d - 2)] = 1000.0 * (i + 1)
+        r = np.zeros((6, d))
+        r[:, :2] = base
+        c = np.zeros((2, d))
+        c[:, :2] = init
+        rows.append(r + off)
+        cents.append(c + off)
+    return np.concatenate(rows), np.concatenate(cents)
+
+
 CASES = {
     # reference tests' own hand example (test_engine.py:10-22)
     "hand": dict(data=_hand, cfg=dict(k=2, init="given", initial=[[0.0], [10.0]], pruning=False, max_iters=20)),
@@ -60,6 +85,13 @@ CASES = {
                      cfg=dict(k=10, init="kmeanspp", seed=36, pruning=True, max_iters=20)),
     "k50_pruned": dict(data=lambda: mixture(MixtureSpec(20000, 8, 50, 37, "uniform", -3, 3, 0.5, 1.0)),
                        cfg=dict(k=50, seed=37, pruning=True, max_iters=25)),
+    # exact ties with the current centroid in pruned passes: the reference keeps it
+    "tie_pruned": dict(data=lambda: _tie_pruned()[0],
+                       cfg=dict(k=2, init="given", initial=_tie_pruned()[1], pruning=True, max_iters=10)),
+    "tie_pruned_d16": dict(data=lambda: _tie_pruned(12, 16)[0],
+                           cfg=dict(k=24, init="given", initial=_tie_pruned(12, 16)[1], pruning=True, max_iters=10)),
+    "tie_pruned_d5": dict(data=lambda: _tie_pruned(5, 5)[0],
+                          cfg=dict(k=10, init="given", initial=_tie_pruned(5, 5)[1], pruning=True, max_iters=10)),
     # d == DP in {16, 32} with k > 16: the twelve-warp MTI and dense kernels
     "d16_k24_pruned": dict(data=lambda: mixture(MixtureSpec(6000, 16, 24, 38, "uniform", -4, 4, 1.0)),
                            cfg=dict(k=24, seed=38, pruning=True, max_iters=30)),

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("KNB_LIB") or os.path.join(HERE, "libknorb200.so")  # 
 
 KNB_E_ARG, KNB_E_CUDA, KNB_E_STATE, KNB_E_COUNT, KNB_E_NOMEM = -1, -2, -3, -4, -5
 KNB_OPT_MTI_SCAN = 1
-MTI_SCAN = {"auto": 0, "exact": 1, "dense": 2, "block": 3}
+MTI_SCAN = {"auto": 0, "exact": 1, "dense": 2, "block": 3, "tc": 4}
 
 
 class NativeUnavailable(RuntimeError):
@@ -93,6 +93,8 @@ SIGNATURES = {
     "knb_set_stream": [_P, _P],
     "knb_state_bytes": [_P, _PI64],
     "knb_describe": [_P, _PI32, _PI32, _PI32, _PI32],
+    "knb_mti_tc_info": [_P, _PI32, _PI64],
+    "knb_mti_tc_scores": [_P, _P],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
     "knb_block_distances": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _P, _P, _P],
     "knb_rowwise": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _I32, _P],
@@ -122,6 +124,8 @@ def lib():
     h.knb_last_error.argtypes = []
     h.knb_f32_supported.restype = ctypes.c_int
     h.knb_f32_supported.argtypes = [_I32, _I32, _I32]
+    h.knb_mti_compact_ok.restype = ctypes.c_int
+    h.knb_mti_compact_ok.argtypes = [_I64]
     for name, args in SIGNATURES.items():
         fn = getattr(h, name)
         fn.restype = ctypes.c_int
@@ -389,6 +393,15 @@ class Context:
         check(self.L.knb_state_bytes(self.h, ctypes.byref(v)))
         return int(v.value)
 
+    def mti_tc_info(self) -> dict:
+        a, u = ctypes.c_int32(), ctypes.c_int64()
+        check(self.L.knb_mti_tc_info(self.h, ctypes.byref(a), ctypes.byref(u)))
+        return dict(available=bool(a.value), uncertified=int(u.value))
+
+    def mti_tc_scores(self, dev_ptr: int) -> None:
+        """Scores D~ (n_local x N f32, N = k rounded up to 16) of the tcgen05 MTI pass."""
+        check(self.L.knb_mti_tc_scores(self.h, ctypes.c_void_p(dev_ptr)))
+
     def describe(self) -> dict:
         a, b, c, d = (ctypes.c_int32() for _ in range(4))
         check(self.L.knb_describe(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
@@ -399,6 +412,12 @@ class Context:
 def f32_supported(d: int, k: int, pruning: bool) -> bool:
     """Whether f32 rows stay f32 on the device (dense tcgen05 path); else they are upcast."""
     return bool(lib().knb_f32_supported(int(d), int(k), int(bool(pruning))))
+
+
+def mti_compact_ok(n_local: int) -> bool:
+    """Whether a shard of n_local rows may run the compacted MTI kernel (32-bit row
+    indices); larger shards run the block-dense MTI pass (same results)."""
+    return bool(lib().knb_mti_compact_ok(int(n_local)))
 
 
 def device_info(device: int = 0) -> dict:

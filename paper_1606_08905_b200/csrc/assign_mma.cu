@@ -266,10 +266,10 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
         int nid = sc.id;
         double nd, sq = 0.0;
         if constexpr (W12) {
-          nd = exact_winner_stream<DP>(tb, my_r, crow, k, sc.flag, nid);
+          nd = exact_winner_stream<DP>(tb, my_r, crow, k, sc.flag, nid, live ? aa : -1);
           if (live && nid != aa) sq = exact_sq_stream<DP, true>(tb, my_r, nullptr);
         } else {
-          nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr);
+          nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr, live ? aa : -1);
           if (live && nid != aa) sq = row_self_sq<DP>(tb, my_r, d);
         }
         if (live) {

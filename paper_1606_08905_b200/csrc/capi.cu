@@ -94,6 +94,13 @@ struct knb_ctx {
   unsigned long long* tc_counters = nullptr;
   SegArgs seg;
 
+  // f64 rows, d = 16: the split-TF32 tcgen05 MTI pass (mti_tc.cu)
+  int tcx_nx = 0;                  // f64 ring stages, 0 = not applicable
+  CUtensorMap tmX128;              // 128-row boxes of the f64 rows
+  bool tcx_map = false;
+  void* tcx_bimg = nullptr;        // B operand image
+  unsigned long long* tcx_counters = nullptr;
+
   int DP = 0, DPm = 0, half_in_smem = 0;
   int G_dense = 1, G_mti = 1, G_mti_mma = 1;
   int mti_scan = 0;   // KNB_MTI_AUTO / KNB_MTI_EXACT / KNB_MTI_DENSE
@@ -228,6 +235,7 @@ int reset_run(knb_ctx* c) {
   KNB_CUDA(cudaMemsetAsync(c->assign, 0, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
   KNB_CUDA(cudaMemsetAsync(c->run, 0, sizeof(double) * c->L, c->stream));
   if (c->tc_counters) KNB_CUDA(cudaMemsetAsync(c->tc_counters, 0, 4 * sizeof(unsigned long long), c->stream));
+  if (c->tcx_counters) KNB_CUDA(cudaMemsetAsync(c->tcx_counters, 0, sizeof(unsigned long long), c->stream));
   if (c->sem) {  // a new run starts with an empty cache and zero I/O counters
     KNB_CUDA(cudaMemsetAsync(c->semA.io, 0, sizeof(long long) * 4 * c->max_iters, c->stream));
     KNB_CUDA(cudaMemsetAsync(c->semA.cslot, 0xff, sizeof(int32_t) * (c->n_local ? c->n_local : 1), c->stream));
@@ -238,6 +246,7 @@ int reset_run(knb_ctx* c) {
 
 int build_tmap(knb_ctx* c) {
   c->use_tma = 0;
+  c->tcx_map = false;
   if (c->host_registered) return KNB_OK;  // rows in host memory: cp.async gathers, no tensor maps
   if (c->DP == 0 || (c->d & 1) || (reinterpret_cast<uintptr_t>(c->X) & 15) || c->n_local < 1 ||
       c->n_local > 0x7fffffffLL)
@@ -265,6 +274,14 @@ int build_tmap(knb_ctx* c) {
                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r == CUDA_SUCCESS) c->use_tma = 1;
+  c->tcx_map = false;
+  if (c->use_tma && c->tcx_nx > 0) {  // the tcgen05 MTI pass: 128-row boxes, same swizzle
+    cuuint32_t box128[2] = {16u, 128u};
+    r = encode(&c->tmX128, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(c->X), gdim, gstride, box128,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    c->tcx_map = r == CUDA_SUCCESS;
+  }
   return KNB_OK;
 }
 
@@ -480,6 +497,35 @@ DenseArgs dense_args(knb_ctx* c) {
 
 int launch_pass(knb_ctx* c);
 
+// the split-TF32 tcgen05 MTI pass applies: d = 16, k <= 128, HBM rows with a 128-row map
+bool tcx_ready(const knb_ctx* c) {
+  return c->tcx_nx > 0 && c->tcx_map && !c->host_registered && !c->sem && c->n_local > 0;
+}
+
+int launch_tcx(knb_ctx* c, int gate, float* dbg) {
+  KNB_CUDA(launch_mti_tc_prep(c->means, c->k, c->tcx_bimg, c->stream));
+  MtiTcArgs t;
+  t.n = c->n_local;
+  t.d = c->d;
+  t.k = c->k;
+  t.nx = c->tcx_nx;
+  t.gtc = c->G_dense < c->sms ? c->G_dense : c->sms;
+  t.assign = c->assign;
+  t.upper = c->upper;
+  t.tight = c->tight;
+  t.means = c->means;
+  t.drift = c->drift;
+  t.half_min = c->half_min;
+  t.bimg = c->tcx_bimg;
+  t.partials = c->partials;
+  t.ctrl = c->ctrl;
+  t.gate = gate;
+  t.dbg = dbg;
+  t.counters = c->tcx_counters;
+  KNB_CUDA(launch_mti_tc(&c->tmX128, t, c->G_dense, c->stream));
+  return KNB_OK;
+}
+
 SemArgs sem_args(knb_ctx* c) {
   SemArgs s = c->semA;
   s.assign = c->assign;
@@ -536,7 +582,14 @@ int launch_pass(knb_ctx* c) {
   m.cslot = (c->sem && c->host_registered && c->semA.rows_per_part > 0) ? c->semA.cslot : nullptr;
   m.cache = c->semA.cache;
   m.gate = 0;
-  const int mode = c->mti_mma_ok ? c->mti_scan : KNB_MTI_EXACT;
+  int mode = (c->mti_mma_ok || c->mti_scan == KNB_MTI_TC) ? c->mti_scan : KNB_MTI_EXACT;
+  const bool tcx = tcx_ready(c);
+  if (mode == KNB_MTI_TC && !tcx)
+    return fail(KNB_E_ARG, "the tcgen05 MTI pass needs d == 16, k <= 128 and 16-byte aligned rows in HBM");
+  // the compacted kernel's filter uses 32-bit row / block indices: larger shards take a
+  // block MTI pass (64-bit indices, same results)
+  if ((mode == KNB_MTI_AUTO || mode == KNB_MTI_DENSE) && !mti_compact_ok(c->n_local))
+    mode = tcx ? KNB_MTI_TC : KNB_MTI_BLOCK;
   if (mode == KNB_MTI_EXACT) {
     KNB_CUDA(launch_mti(m, c->DPm, c->G_mti, c->stream));
     KNB_CUDA(launch_reduce(c->partials, c->G_mti, c->L, c->exch, c->ctrl, c->stream));
@@ -544,17 +597,26 @@ int launch_pass(knb_ctx* c) {
   }
   DenseArgs a = dense_args(c);
   a.mti_filter = 1;
-  if (mode == KNB_MTI_BLOCK) {
+  if (mode == KNB_MTI_TC) {
+    int rc = launch_tcx(c, 0, nullptr);
+    if (rc) return rc;
+  } else if (mode == KNB_MTI_BLOCK) {
     KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
   } else if (mode == KNB_MTI_DENSE) {
     KNB_CUDA(launch_mti_mma(m, c->DP, c->G_dense, c->stream));
   } else {
     // auto: both are queued; the device-side choice made by the previous finalize
-    // (skip fraction) lets exactly one of them run, the other returns at once
+    // (skip fraction) lets exactly one of them run, the other returns at once.  The
+    // block form is the tcgen05 pass where it applies (d = 16: config 4)
     a.gate = 1;
     m.gate = 1;
-    KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
-    KNB_CUDA(launch_mti_mma(m, c->DP, c->G_dense, c->stream));
+    if (tcx) {
+      int rc = launch_tcx(c, 1, nullptr);
+      if (rc) return rc;
+    } else {
+      KNB_CUDA(launch_dense(&c->tmap, a, c->DP, c->G_dense, c->stream));
+    }
+    if (mti_compact_ok(c->n_local)) KNB_CUDA(launch_mti_mma(m, c->DP, c->G_dense, c->stream));
   }
   KNB_CUDA(launch_reduce(c->partials, c->G_dense, c->L, c->exch, c->ctrl, c->stream));
   return KNB_OK;
@@ -727,6 +789,7 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     c->G_mti = (int)(tiles < g ? tiles : g);
   }
   c->mti_mma_ok = c->DP != 0 && mti_mma_fits(c->DP, k, d);
+  c->tcx_nx = c->pruning ? mti_tc_stages(d, k) : 0;
   {
     const long long tiles = (nl + 31) / 32;
     c->G_mti_mma = (int)(tiles < c->sms ? tiles : c->sms);
@@ -742,6 +805,12 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     if ((rc = dev_alloc(c, &c->half, (size_t)k * k))) return bail(rc);
     if ((rc = dev_alloc(c, &c->half_min, k))) return bail(rc);
     if (cudaMemsetAsync(c->tight, 0, nl, c->stream) != cudaSuccess) return bail(fail(KNB_E_CUDA, "memset"));
+  }
+  if (c->tcx_nx > 0) {
+    if ((rc = dev_alloc(c, &c->tcx_counters, 1))) return bail(rc);
+    double* bimg = nullptr;
+    if ((rc = dev_alloc(c, &bimg, mti_tc_bimg_bytes(k) / sizeof(double)))) return bail(rc);
+    c->tcx_bimg = bimg;
   }
   if ((rc = dev_alloc(c, &c->run, c->L))) return bail(rc);
   if ((rc = dev_alloc(c, &c->means, kd))) return bail(rc);
@@ -774,7 +843,7 @@ int knb_destroy(knb_ctx* c) {
   void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
                   c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->fin_sync, c->stats,
                   c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
-                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->seg.counts,
+                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->tcx_bimg, c->tcx_counters, c->seg.counts,
                   c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records,
                   c->semA.fetched, c->semA.cslot, c->semA.crow, c->semA.cache, c->semA.bcount, c->semA.bpre,
                   c->semA.plo, c->semA.io};
@@ -790,6 +859,8 @@ int knb_destroy(knb_ctx* c) {
 }
 
 int knb_f32_supported(int32_t d, int32_t k, int32_t pruning) { return f32_supported(d, k, pruning) ? 1 : 0; }
+
+int knb_mti_compact_ok(int64_t n_local) { return mti_compact_ok(n_local) ? 1 : 0; }
 
 int knb_upload_rows_f32(knb_ctx* c, const float* host, int64_t lo, int64_t rows) {
   if (!c || (!host && rows > 0)) return fail(KNB_E_ARG, "null argument");
@@ -827,6 +898,30 @@ int knb_tc_info(knb_ctx* c, int32_t* active, int64_t* flagged, int64_t* full_rer
   }
   if (flagged) *flagged = (int64_t)h[1];
   if (full_reranks) *full_reranks = (int64_t)h[2];
+  return KNB_OK;
+}
+
+int knb_mti_tc_info(knb_ctx* c, int32_t* available, int64_t* uncertified) {
+  if (!c) return fail(KNB_E_ARG, "null context");
+  if (available) *available = tcx_ready(c) ? 1 : 0;
+  unsigned long long h = 0;
+  if (c->tcx_counters) {
+    KNB_CUDA(cudaSetDevice(c->device));
+    KNB_CUDA(cudaMemcpyAsync(&h, c->tcx_counters, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (uncertified) *uncertified = (int64_t)h;
+  return KNB_OK;
+}
+
+int knb_mti_tc_scores(knb_ctx* c, float* dev_out) {
+  int rc = need_ready(c, true);
+  if (rc) return rc;
+  if (!tcx_ready(c)) return fail(KNB_E_STATE, "the tcgen05 MTI pass does not apply to this context");
+  if (!dev_out) return fail(KNB_E_ARG, "null output");
+  if ((rc = ensure_partials(c))) return rc;
+  if ((rc = launch_tcx(c, 0, dev_out))) return rc;
+  KNB_CUDA(cudaStreamSynchronize(c->stream));
   return KNB_OK;
 }
 
@@ -1415,7 +1510,9 @@ int knb_set_ignore_stop(knb_ctx* c, int32_t on) {
 int knb_set_option(knb_ctx* c, int32_t option, int64_t value) {
   if (!c) return fail(KNB_E_ARG, "null context");
   if (option == KNB_OPT_MTI_SCAN) {
-    if (value < KNB_MTI_AUTO || value > KNB_MTI_BLOCK) return fail(KNB_E_ARG, "bad MTI scan mode");
+    if (value < KNB_MTI_AUTO || value > KNB_MTI_TC) return fail(KNB_E_ARG, "bad MTI scan mode");
+    if (value == KNB_MTI_TC && c->tcx_nx == 0)
+      return fail(KNB_E_ARG, "the tcgen05 MTI pass needs a pruned run with d == 16 and k <= 128");
     if ((value == KNB_MTI_DENSE || value == KNB_MTI_BLOCK) && !c->mti_mma_ok)
       return fail(KNB_E_ARG, "dense MTI scan needs d <= 64 and centroids that fit shared memory");
     c->mti_scan = (int)value;

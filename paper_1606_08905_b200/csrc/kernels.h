@@ -162,6 +162,31 @@ cudaError_t launch_row_sqnorm_f32(const float* X, long long n, int d, double* ou
 cudaError_t launch_tc_scalars(const unsigned long long* counters, long long n_local, int k, int d,
                               double* exch, const Ctrl* ctrl, cudaStream_t s);
 
+// f64 rows (d = 16) on the tcgen05 tensor cores: the MTI block pass with split-TF32
+// scores and a certified argmin (mti_tc.cu)
+struct MtiTcArgs {
+  long long n;
+  int d, k;
+  int nx;                // f64 ring stages (mti_tc_stages)
+  int gtc;               // CTAs that take tiles (<= gridDim.x; the rest write zero partials)
+  int32_t* assign;
+  double* upper;
+  uint8_t* tight;
+  const double* means;   // k x 16
+  const double* drift;
+  const double* half_min;
+  const void* bimg;      // B operand image (launch_mti_tc_prep)
+  double* partials;
+  const Ctrl* ctrl;
+  int gate;              // run only when ctrl->mti_choice == 1
+  float* dbg;            // non-null: dump the n x N scores D~ and change nothing
+  unsigned long long* counters;  // [0] uncertified (re-ranked) rows, cumulative
+};
+int mti_tc_stages(int d, int k);
+size_t mti_tc_bimg_bytes(int k);
+cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, cudaStream_t s);
+cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s);
+
 // deterministic cluster-sorted accumulation (segsum.cu)
 struct SegArgs {
   const void* X;         // f32 or f64 rows
@@ -198,6 +223,7 @@ size_t mti_tile_smem(int DP, int k, int half_in_smem);
 cudaError_t launch_dense(const CUtensorMap* tmap, const DenseArgs& a, int DP, int grid, cudaStream_t s);
 cudaError_t launch_mti(const MtiArgs& a, int DP, int grid, cudaStream_t s);
 bool mti_mma_fits(int DP, int k, int d);
+bool mti_compact_ok(long long n_local);
 cudaError_t launch_mti_mma(const MtiArgs& a, int DP, int grid, cudaStream_t s);
 int dense_tile_grid(int DP, int k, int d, int sms);  // CTAs per device for the tensor-core path
 int mti_tile_grid(int DP, int k, int half_in_smem, int sms);

@@ -287,9 +287,13 @@ __device__ __forceinline__ Scored rows_to_lanes(const Scored& sc, int lane) {
 
 // Exact recipe on the lane's row: re-rank over every centroid (ascending, strict <,
 // sqrt domain, distance.py:106-116) when flagged, else the distance to `id`.
+// orig >= 0 (pruned passes): the scan starts from the point's current centroid and its
+// exact distance and skips it, as scan_block does (pruning.py:174-203: cur = orig,
+// switch only on dx < u), so an exact tie keeps the current centroid; orig < 0 (full
+// passes, nearest_block_into): the lowest id wins a tie.
 template <int DP, class TL = TileLayout<DP>>
 __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, const double* crow, int k, int d,
-                                               bool flag, int& id, double* sq_out) {
+                                               bool flag, int& id, double* sq_out, int orig = -1) {
   double x[DP];
 #pragma unroll
   for (int q2 = 0; q2 < DP / 2; ++q2) {
@@ -299,17 +303,20 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
   }
   double nd;
   if (flag) {
-    double bd = CUDART_INF;
-    int bi = 0;
-    for (int j = 0; j < k; ++j) {
-      double dj;
+    auto dist = [&](int j) {
       if constexpr (DP <= 32) {
         double cj[DP];
         load_crow<DP>(crow, j, cj);
-        dj = sqrt(exact_sq<DP>(x, cj, d));
+        return sqrt(exact_sq<DP>(x, cj, d));
       } else {
-        dj = sqrt(exact_sq<DP>(x, crow + j * crow_stride<DP>(), d));
+        return sqrt(exact_sq<DP>(x, crow + j * crow_stride<DP>(), d));
       }
+    };
+    double bd = orig >= 0 ? dist(orig) : CUDART_INF;
+    int bi = orig >= 0 ? orig : 0;
+    for (int j = 0; j < k; ++j) {
+      if (j == orig) continue;
+      const double dj = dist(j);
       if (dj < bd) { bd = dj; bi = j; }
     }
     id = bi;
@@ -376,14 +383,16 @@ __device__ __forceinline__ double exact_sq_stream(const unsigned char* tb, int r
   return __dadd_rn(__dadd_rn(s[0], s[2]), __dadd_rn(s[1], s[3]));
 }
 
-// exact_winner for d == DP with the streamed tree (fewest registers)
+// exact_winner for d == DP with the streamed tree (fewest registers); same orig rule
 template <int DP, class TL = TileLayout<DP>>
 __device__ __forceinline__ double exact_winner_stream(const unsigned char* tb, int r, const double* crow, int k,
-                                                      bool flag, int& id) {
+                                                      bool flag, int& id, int orig = -1) {
   if (flag) {
-    double bd = CUDART_INF;
-    int bi = 0;
+    double bd = orig >= 0 ? sqrt(exact_sq_stream<DP, false, TL>(tb, r, crow + orig * crow_stride<DP>()))
+                          : CUDART_INF;
+    int bi = orig >= 0 ? orig : 0;
     for (int j = 0; j < k; ++j) {
+      if (j == orig) continue;
       const double dj = sqrt(exact_sq_stream<DP, false, TL>(tb, r, crow + j * crow_stride<DP>()));
       if (dj < bd) { bd = dj; bi = j; }
     }

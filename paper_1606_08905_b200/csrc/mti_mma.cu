@@ -5,10 +5,12 @@
 // (pruning.py:152-160) + scan_block (pruning.py:163-204) with these semantics:
 //   prologue  u += drift[a]; tight &= (drift[a] == 0)        (bound inflation, fused)
 //   clause 1  the point is skipped when u <= half_min[a]      (inclusive; its row is never read)
-//   survivor  its new centroid is the exhaustive argmin (exactly what the reference's
-//             candidate scan returns -- pruning is sound and its distances are the exact
-//             recipe), its bound becomes the exact-recipe distance to that centroid and
-//             tight = 1, as in scan_block; moved points contribute signed deltas.
+//   survivor  its new centroid is the exhaustive argmin with scan_block's tie rule (an
+//             exact tie keeps the current centroid, otherwise the lowest id wins: what the
+//             reference's candidate scan returns -- pruning is sound and its distances are
+//             the exact recipe), its bound becomes the exact-recipe distance to that
+//             centroid and tight = 1, as in scan_block; moved points contribute signed
+//             deltas.
 // Assignments, bounds (and therefore every later skip decision), centroids and the
 // skip counts are the reference's; dist_comps counts the k distances evaluated per
 // survivor instead of the reference's clause-2/3 candidate walk (pruned_* are 0).  The
@@ -176,8 +178,8 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
     const int r = lane;  // lane r handles row r from here on
     const bool valid = r < cnum;
     int id = sc.id;
-    const double nd = exact_winner<DP, TL>(tb, r, crow, k, d, sc.flag, id, nullptr);
     const int orig = valid ? qorig[ring(r)] : 0;
+    const double nd = exact_winner<DP, TL>(tb, r, crow, k, d, sc.flag, id, nullptr, valid ? orig : -1);
     const bool moved = valid && id != orig;
     // ||x||^2 only for the (few) moved rows whose signed deltas carry it
     const double sq = moved ? row_self_sq<DP, TL>(tb, r, d) : 0.0;
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
   // filter strided blocks (bound inflation + clause 1) until `target` survivors are queued.
   // The per-row state of the NEXT group of FB blocks is loaded while the current group is
   // filtered (and across calls), so the loads' latency overlaps useful work.  Row and
-  // block indices are 32-bit (the launcher only runs shards below 2^31 - 2^26 rows).
+  // block indices are 32-bit (launch_pass runs this kernel only when mti_compact_ok).
   const int n32 = (int)a.n, nblk32 = (n32 + BR - 1) / BR, TW32 = (int)TW;
   int blk = (int)gw;
   const int32_t* __restrict__ g_assign = a.assign;
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(KNB_W12_THREADS, 1) mti_w12_kernel(const MtiAr
     const Scored sc = score_block<DP, false, true, true, true, TL>(tb, crow, chn, ntile8, tolk, cmax2, lane, xb);
     int id = __shfl_sync(0xffffffffu, sc.id, owner_lane(r));
     const bool flag = __shfl_sync(0xffffffffu, (int)sc.flag, owner_lane(r)) != 0;
-    const double nd = exact_winner_stream<DP, TL>(tb, r, crow, k, flag, id);
+    const double nd = exact_winner_stream<DP, TL>(tb, r, crow, k, flag, id, valid ? orig : -1);
     const bool moved = valid && id != orig;
     const double sq = moved ? exact_sq_stream<DP, true, TL>(tb, r, nullptr) : 0.0;
     if (valid) {
@@ -614,6 +616,10 @@ cudaError_t launch_dp(const MtiArgs& a, int grid, cudaStream_t s) {
 }  // namespace
 
 bool mti_mma_fits(int DP, int k, int d) { return DP >= 4 && DP <= 64 && mti_warps_for(DP, k, d) > 0; }
+
+// the compacted kernels' filter walks 32-bit row / block indices (blk may run FB * TW
+// blocks past the end): shards up to 2^31 - 2^26 rows
+bool mti_compact_ok(long long n_local) { return n_local <= (1LL << 31) - (1LL << 26); }
 
 cudaError_t launch_mti_mma(const MtiArgs& a, int DP, int grid, cudaStream_t s) {
   switch (DP) {

@@ -29,7 +29,8 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert lib.knb_version() == 1
     # every declared symbol has a Python binding signature (or is version/last_error)
-    unbound = [n for n in names if n not in _native.SIGNATURES and n not in ("knb_version", "knb_last_error", "knb_f32_supported")]
+    unbound = [n for n in names if n not in _native.SIGNATURES and n not in ("knb_version", "knb_last_error", "knb_f32_supported",
+                                                                          "knb_mti_compact_ok")]
     assert not unbound, unbound
 
 
@@ -62,3 +63,13 @@ def test_f32_path_rule():
     assert not _native.f32_supported(16, 8, False)
     assert not _native.f32_supported(258, 8, False)
     assert not _native.f32_supported(260, 8, False)
+
+
+def test_compacted_mti_kernel_dispatch_guard():
+    """The compacted MTI kernel's filter uses 32-bit row indices: shards above
+    2^31 - 2^26 rows must be routed to the block-dense pass."""
+    from paper_1606_08905_b200 import _native
+    assert _native.mti_compact_ok(856_000_000)
+    assert _native.mti_compact_ok((1 << 31) - (1 << 26))
+    assert not _native.mti_compact_ok((1 << 31) - (1 << 26) + 1)
+    assert not _native.mti_compact_ok(3_000_000_000)
