@@ -220,6 +220,12 @@ int knb_mti_tc_info(knb_ctx* ctx, int32_t* available, int64_t* uncertified);
 /* Test hook: the pass's split-TF32 scores D~ (n_local x N floats, N = k rounded up to 16,
  * ~ ||x - c_j||^2) against the current centroids, into device memory; no state changes. */
 int knb_mti_tc_scores(knb_ctx* ctx, float* dev_out);
+/* Profiling builds (-DKNB_TCX_PROF=1): cycles each role of the tcgen05 MTI kernel spent
+ * waiting / working, summed over CTAs since the last call (then cleared); *enabled = 0 and
+ * zeros in normal builds.  Slots: producer [0 wait x_empty, 1 issue], issuer [2 wait A,
+ * 3 wait TMEM, 4 issue], converter [5 wait x_full, 6 wait A slot, 7 work], epilogue [8 wait
+ * TMEM full, 9 keys, 10 wait rows, 11 certify + bound + state, 12 accumulate, 13 other]. */
+int knb_mti_tc_prof(int64_t* out16, int32_t* enabled);
 
 /* numpy's default_rng(seed).random(...) on the device: writes draws [first_draw,
  * first_draw + count) of the PCG64 stream whose (state, inc) the host read from

@@ -95,6 +95,7 @@ SIGNATURES = {
     "knb_describe": [_P, _PI32, _PI32, _PI32, _PI32],
     "knb_mti_tc_info": [_P, _PI32, _PI64],
     "knb_mti_tc_scores": [_P, _P],
+    "knb_mti_tc_prof": [_PI64, _PI32],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
     "knb_block_distances": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _P, _P, _P],
     "knb_rowwise": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _I32, _P],
@@ -418,6 +419,14 @@ def mti_compact_ok(n_local: int) -> bool:
     """Whether a shard of n_local rows may run the compacted MTI kernel (32-bit row
     indices); larger shards run the block-dense MTI pass (same results)."""
     return bool(lib().knb_mti_compact_ok(int(n_local)))
+
+
+def mti_tc_prof() -> tuple[bool, list[int]]:
+    """(enabled, 16 cycle counters) of a -DKNB_TCX_PROF=1 build; read and cleared."""
+    out = (ctypes.c_int64 * 16)()
+    en = ctypes.c_int32()
+    check(lib().knb_mti_tc_prof(out, ctypes.byref(en)))
+    return bool(en.value), [int(v) for v in out]
 
 
 def device_info(device: int = 0) -> dict:

@@ -99,6 +99,7 @@ struct knb_ctx {
   CUtensorMap tmX128;              // 128-row boxes of the f64 rows
   bool tcx_map = false;
   void* tcx_bimg = nullptr;        // B operand image
+  unsigned char* tcx_recs = nullptr;  // per-tile moved-row records (mti_tc_delta_kernel)
   unsigned long long* tcx_counters = nullptr;
 
   int DP = 0, DPm = 0, half_in_smem = 0;
@@ -505,6 +506,7 @@ bool tcx_ready(const knb_ctx* c) {
 int launch_tcx(knb_ctx* c, int gate, float* dbg) {
   KNB_CUDA(launch_mti_tc_prep(c->means, c->k, c->tcx_bimg, c->stream));
   MtiTcArgs t;
+  t.X = c->X;
   t.n = c->n_local;
   t.d = c->d;
   t.k = c->k;
@@ -522,7 +524,10 @@ int launch_tcx(knb_ctx* c, int gate, float* dbg) {
   t.gate = gate;
   t.dbg = dbg;
   t.counters = c->tcx_counters;
+  t.kmask = 0xFFFFFF80u;
+  t.recs = c->tcx_recs;
   KNB_CUDA(launch_mti_tc(&c->tmX128, t, c->G_dense, c->stream));
+  if (!dbg) KNB_CUDA(launch_mti_tc_delta(t, c->G_dense, c->stream));
   return KNB_OK;
 }
 
@@ -811,6 +816,10 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     double* bimg = nullptr;
     if ((rc = dev_alloc(c, &bimg, mti_tc_bimg_bytes(k) / sizeof(double)))) return bail(rc);
     c->tcx_bimg = bimg;
+    double* recs = nullptr;
+    const size_t rec_bytes = (size_t)((nl + 127) / 128) * TC_REC;
+    if ((rc = dev_alloc(c, &recs, (rec_bytes + 7) / 8))) return bail(rc);
+    c->tcx_recs = reinterpret_cast<unsigned char*>(recs);
   }
   if ((rc = dev_alloc(c, &c->run, c->L))) return bail(rc);
   if ((rc = dev_alloc(c, &c->means, kd))) return bail(rc);
@@ -843,7 +852,7 @@ int knb_destroy(knb_ctx* c) {
   void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
                   c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->fin_sync, c->stats,
                   c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
-                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->tcx_bimg, c->tcx_counters, c->seg.counts,
+                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->tcx_bimg, c->tcx_recs, c->tcx_counters, c->seg.counts,
                   c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records,
                   c->semA.fetched, c->semA.cslot, c->semA.crow, c->semA.cache, c->semA.bcount, c->semA.bpre,
                   c->semA.plo, c->semA.io};
@@ -911,6 +920,16 @@ int knb_mti_tc_info(knb_ctx* c, int32_t* available, int64_t* uncertified) {
     KNB_CUDA(cudaStreamSynchronize(c->stream));
   }
   if (uncertified) *uncertified = (int64_t)h;
+  return KNB_OK;
+}
+
+int knb_mti_tc_prof(int64_t* out16, int32_t* enabled) {
+  if (!out16) return fail(KNB_E_ARG, "null output");
+  unsigned long long h[16];
+  const int rc = mti_tc_prof(h);
+  if (rc < 0) return fail(KNB_E_CUDA, "reading the tcgen05 MTI profile counters");
+  for (int i = 0; i < 16; ++i) out16[i] = (int64_t)h[i];
+  if (enabled) *enabled = rc;
   return KNB_OK;
 }
 

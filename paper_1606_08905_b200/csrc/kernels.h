@@ -165,6 +165,7 @@ cudaError_t launch_tc_scalars(const unsigned long long* counters, long long n_lo
 // f64 rows (d = 16) on the tcgen05 tensor cores: the MTI block pass with split-TF32
 // scores and a certified argmin (mti_tc.cu)
 struct MtiTcArgs {
+  const double* X;       // n x 16 rows (the epilogue's exact recipe reads them through L2)
   long long n;
   int d, k;
   int nx;                // f64 ring stages (mti_tc_stages)
@@ -181,8 +182,13 @@ struct MtiTcArgs {
   int gate;              // run only when ctrl->mti_choice == 1
   float* dbg;            // non-null: dump the n x N scores D~ and change nothing
   unsigned long long* counters;  // [0] uncertified (re-ranked) rows, cumulative
+  uint32_t kmask;        // 0xFFFFFF80 (key mask, passed at run time)
+  unsigned char* recs;   // per 128-row tile: moved-row masks (4 x u32) + old ids (u8 x 128)
 };
+constexpr int TC_REC = 16 + 128;
+cudaError_t launch_mti_tc_delta(const MtiTcArgs& a, int grid, cudaStream_t s);
 int mti_tc_stages(int d, int k);
+int mti_tc_prof(unsigned long long* out);  // 16 counters; returns 1 in a -DKNB_TCX_PROF=1 build
 size_t mti_tc_bimg_bytes(int k);
 cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, cudaStream_t s);
 cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s);
