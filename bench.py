@@ -3,8 +3,10 @@
 
 A step is one Lloyd iteration over every point of the workload (assign or MTI
 filter/scan + accumulate, the cross-GPU exchange, finalize).  Default workload
-= BASELINE.json configs[1] ("c2"): n = 2,000,000, d = 32, k = 32, float64,
-mixture of 32 Gaussians, kmeans++ init, MTI pruning on.  W warm-up iterations
+= BASELINE.json configs[3] ("c4", the north star's config and the largest one
+that fits one B200): n = 856,000,000, d = 16, k = 100, float64, i.i.d.
+U[0,1)^16 from default_rng(4) (generated in HBM by the PCG64 kernel, bit-identical
+to numpy's stream), forgy init, MTI pruning on.  W warm-up iterations
 run first (iteration 0 is the dense full pass), then exactly K iterations are
 timed with CUDA events on the launching stream, bracketed by barrier +
 synchronize, max over ranks.  The run keeps iterating after convergence (every
@@ -57,12 +59,16 @@ def load_peaks():
 
 def measured_traffic(config: str):
     """DRAM bytes (read + write) per launch of the config's dominant kernel from the
-    committed ncu capture (profiles/r01_traffic.json), or None."""
-    try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as fh:
-            t = json.load(fh).get(config)
-    except (OSError, ValueError):
-        return None, None
+    committed ncu capture (profiles/r02_traffic.json, else r01), or None."""
+    t = None
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", f"{rnd}_traffic.json")) as fh:
+                t = json.load(fh).get(config)
+        except (OSError, ValueError):
+            t = None
+        if t:
+            break
     if not t:
         return None, None
     return t["traffic_bytes"], f"{t['kernel']}: {t['source']}"
@@ -182,10 +188,13 @@ def cpu_baseline(name, cfg, warmup, steps):
     walls, r = cpu_port_run(name, cfg, n_sub, warmup + steps, threads)
     timed = walls[warmup:warmup + steps] or walls
     value = n_sub * len(timed) / sum(timed)
+    rows = (f"the first {n_sub} rows of the {name} stream (default_rng(4).random is prefix-consistent)"
+            if name == "c4" else
+            f"{n_sub} rows drawn from the {name} law with its seed (a sub-scale instance: the mixtures "
+            f"draw labels before noise, so they are not prefix-consistent)")
     return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle/lloyd.py (restatement pinned bit-exact to numakmeans) on the first "
-                      f"{n_sub} rows of the {name} law, iterations {warmup}..{warmup + len(timed) - 1} "
-                      f"after the same init, {threads} threads"}
+            "sample": f"oracle/lloyd.py (restatement pinned bit-exact to numakmeans) on {rows}, its own "
+                      f"{cfg['init']} init, iterations {warmup}..{warmup + len(timed) - 1}, {threads} threads"}
 
 
 def run_reference(args):
@@ -237,10 +246,9 @@ def run_ours(args):
         dev_rows = kb.synth.uniform_device(n, 16, 4, row_lo=lo, rows=hi - lo, device=local_rank)
         host = None
         d = 16
-        args.no_e2e = True
     elif name == "c5":
         # 10 GB of f32 rows: the mixture law generated in HBM (torch's seeded generator);
-        # the e2e leg copies it to pinned host memory first
+        # the e2e leg copies it to a pageable host array first
         spec = cfg["spec"](hi - lo)
         dev_rows = kb.synth.mixture_device(spec, device=local_rank)
         host = None
@@ -350,10 +358,28 @@ def run_ours(args):
     fp_peak = tf32_peak if tc else 2 * dfma_peak
     t_fp = flops / fp_peak
     t_hbm = bytes_ / (hbm_peak * 1e9)
+    tcx = (not tc) and cfg["pruning"] and run.ctx.mti_tc_info()["available"]  # f64 rows, tcgen05 MTI pass
     if tc:
         roof = {"bound": "tensor", "achieved": flops / kern_s / 1e12, "peak": fp_peak / 1e12,
                 "unit": "TFLOP/s", "peak_source": "0.5 x MEASURED_PEAKS.json bf16_tflops (kind::tf32 = half the "
                                                   "bf16 rate)"}
+    elif tcx:
+        # split-TF32 scores on the tensor cores (mti_tc.cu): the FP64 FMA peak no longer
+        # bounds the pass; its roofline is the slower of the point bytes over HBM and the
+        # TF32 tensor work (seven K = 8 UMMAs per 128 rows over k rounded up to 16 columns)
+        n16 = (k + 15) // 16 * 16
+        t_tf = 2.0 * n_loc * n16 * 56 / tf32_peak
+        if t_hbm >= t_tf:
+            roof = {"bound": "hbm", "achieved": bytes_ / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        else:
+            roof = {"bound": "tensor", "achieved": 2.0 * n_loc * n16 * 56 / kern_s / 1e12, "peak": tf32_peak / 1e12,
+                    "unit": "TFLOP/s", "peak_source": "0.5 x MEASURED_PEAKS.json bf16_tflops"}
+        roof["fp64_equivalent"] = {"achieved_TFLOPs": flops / kern_s / 1e12, "fp64_peak_TFLOPs": 2 * dfma_peak / 1e12,
+                                   "frac": flops / kern_s / (2 * dfma_peak),
+                                   "note": "the north star's FP64 roofline (n*k*d FMAs at the measured FP64 peak), "
+                                           "which the tensor-core pass exceeds"}
+        roof["uncertified_rows"] = run.ctx.mti_tc_info()["uncertified"]
     elif t_fp >= t_hbm:
         roof = {"bound": "fp64", "achieved": flops / kern_s / 1e12, "peak": 2 * dfma_peak / 1e12,
                 "unit": "TFLOP/s", "peak_source": "measured in-run DFMA microbenchmark (knb_measure_peaks)"}
@@ -363,6 +389,7 @@ def run_ours(args):
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"], roof["traffic_source"] = measured_traffic(args.config)
     roof["kernel"] = ("tc_assign_kernel + tc_rerank + segsum" if tc else
+                      "mti_tc_kernel (tcgen05 split-TF32) + mti_tc_delta_kernel + reduce" if tcx else
                       "mti_mma_kernel (compacted survivors) + reduce" if cfg["pruning"] else
                       "dense_mma_kernel + reduce")
     roof["kernel_ms"] = kern_s * 1e3
@@ -389,6 +416,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         k1_s = statistics.mean(a.elapsed_time(b) for a, b in kev) * 1e-3
         dense.close()
+        del dense
         roof_k1 = {"bound": "tensor" if tc else "fp64" if t_fp >= t_hbm else "hbm",
                    "kernel": "tc_assign_kernel + tc_rerank + segsum" if tc else "dense_tile_kernel + reduce",
                    "kernel_ms": k1_s * 1e3, "dense_dp": desc["dense_dp"], "tma": desc["tma"]}
@@ -401,6 +429,7 @@ def run_ours(args):
         roof_k1["fp64_TFLOPs" if not tc else "tf32_TFLOPs"] = flops / k1_s / 1e12
     tcinfo = run.ctx.tc_info() if tc else None
     run.close()
+    del run  # (it holds the device rows; the e2e leg needs their HBM back)
 
     # the sampler covers the timed region; stopped before the e2e leg, whose CUDA calls
     # (allocation, page-locking) nvidia-smi's polling would otherwise contend with
@@ -411,10 +440,9 @@ def run_ours(args):
     if world == 1 and not args.no_e2e:
         ecfg2 = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=cfg["pruning"],
                                 max_iters=cfg["max_iters"], tolerance=cfg["tolerance"], device=local_rank)
-        # the user's rows in pinned host memory (H2D at full PCIe/C2C speed)
-        pinned = torch.empty(tuple(dev_rows.shape), dtype=dev_rows.dtype, pin_memory=True)
-        pinned.copy_(dev_rows if host is None else torch.from_numpy(host))
-        host = pinned.numpy()
+        # the user's rows in an ordinary (pageable) numpy array, as a caller holds them
+        if host is None:
+            host = dev_rows.cpu().numpy()
         del dev_rows
         torch.cuda.empty_cache()
         kb.kmeans(host[: min(n, 100_000)], ecfg2)  # warm-up (context + modules)
@@ -437,7 +465,9 @@ def run_ours(args):
 
     # kernels per step: K1/MTI pass + CTA merge + finalize + stats (+ geometry when pruning);
     # tcgen05 path: prep, assign, rerank, 6 segsum stages, scalars, finalize, stats
-    launches_per_step = 12 if tc else 4 + (1 if cfg["pruning"] else 0)
+    # tcgen05 MTI (c4): prep, mti_tc, delta, the gated compacted MTI kernel (returns at once),
+    # reduce, finalize, geometry
+    launches_per_step = 12 if tc else 7 if tcx else 4 + (1 if cfg["pruning"] else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -476,22 +506,46 @@ def _json_stdout():
         pass
 
 
+def relaunch_distributed(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: re-run this command as N ranks (one process
+    per GPU) under torch.distributed.run on 127.0.0.1, and return its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
+    if "WORLD_SIZE" not in os.environ:
+        for i, a in enumerate(sys.argv):  # --gpus N (or --gpus=N) without torchrun: spawn the ranks
+            v = a.split("=", 1)[1] if a.startswith("--gpus=") else (sys.argv[i + 1] if a == "--gpus" and
+                                                                     i + 1 < len(sys.argv) else None)
+            if v is not None and int(v) > 1:
+                return relaunch_distributed(int(v))
     _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n", type=int, default=None, help="override n (rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-reps", type=int, default=2)
+    ap.add_argument("--e2e-reps", type=int, default=None, help="e2e calls (default 2; 1 for c4)")
     ap.add_argument("--mti-scan", default="auto", help="EngineConfig.mti_scan for the timed run (experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 warm-up steps
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if args.e2e_reps is None:
+        args.e2e_reps = 1 if args.config == "c4" else 2
     return run_reference(args) if args.impl == "reference" else run_ours(args)
 
 
