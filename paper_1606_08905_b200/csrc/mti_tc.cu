@@ -84,8 +84,26 @@ constexpr uint32_t A_TILE = A_CHUNK + A_CONST;
 constexpr int PF = KNB_TCX_PF;                 // tiles pulled into L2 ahead of their TMA load
 constexpr int NA = 2;                          // operand stages
 constexpr int TCOLS = 128;                     // TMEM columns per accumulator buffer
-constexpr int THREADS = 448;  // warp 0 TMA, 1 MMA, 2-5 convert, 6-13 epilogue (two groups)
-constexpr int W_CONV = 2, W_EPI = 6;
+#ifndef KNB_TCX_GROUPS
+#define KNB_TCX_GROUPS 3
+#endif
+// warps: 0 TMA, 1 MMA, converters (NCONV), then NGRP epilogue groups of four; sixteen
+// warps (four per scheduler) keep 128 registers per thread (measured: eighteen warps at
+// 96 registers spill and run 1.97 vs 1.44 ms per 20M c4 rows)
+constexpr int NGRP = KNB_TCX_GROUPS;           // epilogue groups = TMEM accumulator buffers
+#ifndef KNB_TCX_CONV
+#define KNB_TCX_CONV 2
+#endif
+constexpr int NCONV = KNB_TCX_CONV;            // converter warps (128 / (32 NCONV) rows per thread)
+#ifndef KNB_TCX_REGS
+#define KNB_TCX_REGS 128
+#endif
+#ifndef KNB_TCX_GB
+#define KNB_TCX_GB 4
+#endif
+constexpr int W_CONV = 2, W_EPI = 2 + NCONV;
+constexpr int THREADS = 32 * (W_EPI + 4 * NGRP);
+constexpr int TALLOC = NGRP <= 2 ? 2 * TCOLS : 4 * TCOLS;  // power-of-two TMEM allocation
 
 __host__ __device__ inline uint32_t al(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -102,7 +120,7 @@ struct TcxSmem {
     hd = o;   o += (uint32_t)k * 16u;
     ebuf = o; o += (uint32_t)nx * XT * 4u;
     o = al(o, 16);
-    bars = o; o += 8 * (2 * nx + 2 * NA + 4) + 16;
+    bars = o; o += 8 * (2 * nx + 2 * NA + 2 * NGRP) + 16;
     total = o + 1024;  // runtime 1024-byte alignment of the dynamic window
   }
 };
@@ -251,7 +269,7 @@ __device__ __forceinline__ void min2_keys(const int (&key)[W], int& gm, int& g2)
 }
 
 template <int NG, int LAST>
-__global__ void __maxnreg__(128)
+__global__ void __maxnreg__(KNB_TCX_REGS)
     mti_tc_kernel(const __grid_constant__ CUtensorMap tmX, const MtiTcArgs a) {
   constexpr int N = 16 * NG;
   pdl_enter();
@@ -269,8 +287,8 @@ __global__ void __maxnreg__(128)
   uint64_t* a_full = bars + 2 * NX;
   uint64_t* a_empty = a_full + NA;
   uint64_t* t_full = a_empty + NA;
-  uint64_t* t_empty = t_full + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint64_t* t_empty = t_full + NGRP;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + NGRP);
   double* crow = reinterpret_cast<double*>(sm + L.crow);
   double2* hd = reinterpret_cast<double2*>(sm + L.hd);
   float* ebuf = reinterpret_cast<float*>(sm + L.ebuf);  // per stage: the rows' certificate bound E
@@ -295,17 +313,17 @@ __global__ void __maxnreg__(128)
       mbar_init(x_empty + s, 4);  // the four epilogue warps of the tile's group
     }
     for (int s = 0; s < NA; ++s) {
-      mbar_init(a_full + s, 4);
+      mbar_init(a_full + s, NCONV);
       mbar_init(a_empty + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NGRP; ++b) {
       mbar_init(t_full + b, 1);
       mbar_init(t_empty + b, 4);
     }
     fence_barrier_init();
   }
   if (warp == 1 && work) {
-    tmem_alloc(tslot, 2 * TCOLS);
+    tmem_alloc(tslot, TALLOC);
     tmem_relinquish();
   }
   if (warp == 0 && lane == 0 && work) prefetch_tmap(&tmX);
@@ -344,11 +362,12 @@ __global__ void __maxnreg__(128)
       const uint32_t b0 = smem_u32(sm + L.b0), b1 = b0 + N * 128;
       ProfClock pc;
       pc.start();
+      int b = 0, bph = 0;  // accumulator buffer of tile i (= its epilogue group) and its phase
       for (int i = 0; i < mine; ++i) {
-        const int sa = i & 1, b = i & 1;  // NA == 2
+        const int sa = i & 1;  // NA == 2
         mbar_sleep(a_full + sa, (i >> 1) & 1);
         pc.lap(0);
-        mbar_sleep(t_empty + b, ((i >> 1) & 1) ^ 1);
+        mbar_sleep(t_empty + b, bph ^ 1);
         pc.lap(1);
         tc_fence_after();
         const uint32_t dt = tmem + b * TCOLS;
@@ -367,12 +386,13 @@ __global__ void __maxnreg__(128)
         umma_commit(a_empty + sa);
         umma_commit(t_full + b);
         pc.lap(2);
+        if (++b == NGRP) { b = 0; bph ^= 1; }
       }
       pc.flush(2, 3, true);
     }
   } else if (warp < W_EPI) {
     // ------------------------------------------------------------ converters
-    const int r = (warp - W_CONV) * 32 + lane;
+    const int r0 = (warp - W_CONV) * 32 + lane;
     const float cmaxf = __double2float_ru(sqrt(a.ctrl->cmax2));
     const float cmax2f = __double2float_ru(a.ctrl->cmax2);
     ProfClock pc;
@@ -387,6 +407,9 @@ __global__ void __maxnreg__(128)
       const unsigned char* xs = sm + L.x0 + s * X_TILE;
       unsigned char* A0 = sm + L.a0 + sa * A_TILE;
       unsigned char* AC = A0 + A_CHUNK;
+#pragma unroll
+      for (int rr = 0; rr < 4 / NCONV; ++rr) {
+      const int r = r0 + rr * 32 * NCONV;
       float hi[XD], lo[XD];
       float n0 = 0.0f, n1 = 0.0f;
 #pragma unroll
@@ -415,6 +438,7 @@ __global__ void __maxnreg__(128)
       const float xnb = xn2 * (1.0f + 0x1p-12f);
       ebuf[s * XT + r] = (0x1p-20f * (12.5f * sqrtf(xnb) * cmaxf + 4.0f * (xnb + cmax2f)) +
                           (8.0f * XD + 32.0f) * 0x1p-53f * (xnb + cmax2f)) * (1.0f + 0x1p-10f);
+      }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full + sa);
@@ -431,6 +455,7 @@ __global__ void __maxnreg__(128)
     const int q = warp & 3;          // TMEM lane quarter
     const int r = q * 32 + lane;     // row within the tile
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(grp * TCOLS);
+    int tph = 0;  // phase of this group's accumulator buffer
     auto state = [&](int i, int& av, double& uv) {
       const long long row = (long long)(t0 + i * tstep) * XT + r;
       const bool ok = i < mine && row < a.n;
@@ -442,12 +467,12 @@ __global__ void __maxnreg__(128)
     state(grp, pa, pu);
     ProfClock pc;
     pc.start();
-    int s = grp, ph = 0;  // f64 stage of tile i and its phase
-    for (int i = grp; i < mine; i += 2) {
+    int s = grp % NX, ph = grp / NX;  // f64 stage of tile i and its phase
+    for (int i = grp; i < mine; i += NGRP) {
       const long long row = (long long)(t0 + i * tstep) * XT + r;
       const int orig = pa;
       const double u0 = pu;
-      state(i + 2, pa, pu);
+      state(i + NGRP, pa, pu);
       const bool valid = orig >= 0;
       const int oc = valid ? orig : 0;
       const double2 dh = hd[oc];                  // {drift, half_min}
@@ -462,7 +487,8 @@ __global__ void __maxnreg__(128)
         }
       }
       pc.lap(5);
-      mbar_sleep(t_full + grp, (uint32_t)((i >> 1) & 1));
+      mbar_sleep(t_full + grp, (uint32_t)tph);
+      tph ^= 1;
       pc.lap(0);
       tc_fence_after();
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
@@ -485,7 +511,7 @@ __global__ void __maxnreg__(128)
           // group reads only LAST columns (k <= 16 (NG - 1) + LAST)
           const uint32_t kmask = a.kmask;  // 0xFFFFFF80, opaque to ptxas: the column stays the immediate
           int gmv[NG], g2v[NG];
-          constexpr int GB = NG <= 4 ? NG : (NG + 1) / 2;  // groups per TMEM batch
+          constexpr int GB = NG <= KNB_TCX_GB ? NG : KNB_TCX_GB;  // groups per TMEM batch
           uint32_t v[GB][16];
           auto group = [&](auto gc, const uint32_t(&vv)[16]) {
             constexpr int g = decltype(gc)::value;
@@ -501,18 +527,19 @@ __global__ void __maxnreg__(128)
             constexpr int g = decltype(gc)::value;
             tmem_ld<g == NG - 1 ? LAST : 16>(tl + 16 * g, vv);
           };
-          for_groups<GB>([&](auto gc) { load(gc, v[decltype(gc)::value]); });
-          tmem_wait_ld();
-          for_groups<GB>([&](auto gc) { group(gc, v[decltype(gc)::value]); });
-          if constexpr (NG > GB) {
-            for_groups<NG - GB>([&](auto gc) {
-              load(std::integral_constant<int, GB + decltype(gc)::value>{}, v[decltype(gc)::value]);
+          // batches of GB groups: load, one wait, reduce (bounds the registers held)
+          constexpr int NB = (NG + GB - 1) / GB;
+          for_groups<NB>([&](auto bc) {
+            constexpr int B0 = decltype(bc)::value * GB;
+            constexpr int NBG = NG - B0 < GB ? NG - B0 : GB;
+            for_groups<NBG>([&](auto gc) {
+              load(std::integral_constant<int, B0 + decltype(gc)::value>{}, v[decltype(gc)::value]);
             });
             tmem_wait_ld();
-            for_groups<NG - GB>([&](auto gc) {
-              group(std::integral_constant<int, GB + decltype(gc)::value>{}, v[decltype(gc)::value]);
+            for_groups<NBG>([&](auto gc) {
+              group(std::integral_constant<int, B0 + decltype(gc)::value>{}, v[decltype(gc)::value]);
             });
-          }
+          });
 #pragma unroll
           for (int g = 0; g < NG; ++g) k1 = min(k1, gmv[g]);
 #pragma unroll
@@ -606,8 +633,8 @@ __global__ void __maxnreg__(128)
         if ((mm >> lane) & 1u) rb[16 + r] = (unsigned char)orig;
         if (lane == 0) reinterpret_cast<unsigned*>(rb)[q] = mm;
       }
-      s += 2;
-      if (s >= NX) {
+      s += NGRP;
+      while (s >= NX) {
         s -= NX;
         ph ^= 1;
       }
@@ -618,14 +645,14 @@ __global__ void __maxnreg__(128)
   __syncthreads();
   if (warp == 1 && work) {
     tc_fence_after();
-    tmem_dealloc(tmem, 2 * TCOLS);
+    tmem_dealloc(tmem, TALLOC);
   }
 
   // CTA partial: the scalars (mti_tc_delta_kernel writes the sums, counts and sq)
   const long long Lg = acc_len(k, XD);
   double* out = a.partials + (long long)blockIdx.x * Lg;
   const int kk = k * (XD + 2);
-  __shared__ long long red[8][4];
+  __shared__ long long red[4 * NGRP][4];
   if (warp >= W_EPI) {
     const long long c0 = warp_sum_ll(reassigned), c1 = warp_sum_ll(skips), c2 = warp_sum_ll(computed),
                     c3 = warp_sum_ll(flagged);
@@ -640,7 +667,7 @@ __global__ void __maxnreg__(128)
   if (tid == 0) {
     long long tot[4] = {0, 0, 0, 0};
     if (work)
-      for (int w = 0; w < 8; ++w)
+      for (int w = 0; w < 4 * NGRP; ++w)
         for (int c = 0; c < 4; ++c) tot[c] += red[w][c];
     double* sc = out + kk;
     for (int c = 0; c < NSCAL; ++c) sc[c] = 0.0;
