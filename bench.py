@@ -446,6 +446,7 @@ def run_ours(args):
         del dev_rows
         torch.cuda.empty_cache()
         kb.kmeans(host[: min(n, 100_000)], ecfg2)  # warm-up (context + modules)
+        _native.reserve_staging(local_rank)  # the pinned staging pool, once per process
         vals = []
         for _ in range(args.e2e_reps):
             t0 = time.perf_counter()

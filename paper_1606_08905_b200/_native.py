@@ -96,6 +96,7 @@ SIGNATURES = {
     "knb_mti_tc_info": [_P, _PI32, _PI64],
     "knb_mti_tc_scores": [_P, _P],
     "knb_mti_tc_prof": [_PI64, _PI32],
+    "knb_staging_reserve": [ctypes.c_int],
     "knb_measure_peaks": [ctypes.c_int, _PD, _PD],
     "knb_block_distances": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _P, _P, _P],
     "knb_rowwise": [ctypes.c_int, _P, _I64, _P, _I32, _I32, _I32, _P],
@@ -419,6 +420,12 @@ def mti_compact_ok(n_local: int) -> bool:
     """Whether a shard of n_local rows may run the compacted MTI kernel (32-bit row
     indices); larger shards run the block-dense MTI pass (same results)."""
     return bool(lib().knb_mti_compact_ok(int(n_local)))
+
+
+def reserve_staging(device: int = 0) -> None:
+    """Allocate the pinned staging pool for large host transfers now (otherwise the first
+    large kmeans() call of the process pays for pinning it)."""
+    check(lib().knb_staging_reserve(int(device)))
 
 
 def mti_tc_prof() -> tuple[bool, list[int]]:

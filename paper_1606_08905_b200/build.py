@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libknorb200.so")
-SOURCES = ["capi.cu", "assign.cu", "assign_mma.cu", "mti.cu", "mti_mma.cu", "update.cu", "init.cu", "peaks.cu", "pcg64.cu", "assign_tc.cu", "segsum.cu", "sem.cu", "primitives.cu", "mti_tc.cu"]
+SOURCES = ["capi.cu", "assign.cu", "assign_mma.cu", "mti.cu", "mti_mma.cu", "update.cu", "init.cu", "peaks.cu", "pcg64.cu", "assign_tc.cu", "segsum.cu", "sem.cu", "primitives.cu", "mti_tc.cu", "hostcopy.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

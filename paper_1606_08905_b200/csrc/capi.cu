@@ -882,9 +882,10 @@ int knb_upload_rows_f32(knb_ctx* c, const float* host, int64_t lo, int64_t rows)
     if ((rc = tc_attach(c, c->X32_own))) return rc;
   }
   c->xn_valid = false;
-  if (rows)
-    KNB_CUDA(cudaMemcpyAsync(c->X32_own + lo * c->d, host, sizeof(float) * rows * c->d, cudaMemcpyHostToDevice,
-                             c->stream));
+  if (rows) {
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+    KNB_CUDA(staged_copy(c->device, c->X32_own + lo * c->d, host, sizeof(float) * rows * c->d, true));
+  }
   return KNB_OK;
 }
 
@@ -972,9 +973,10 @@ int knb_upload_rows(knb_ctx* c, const double* host, int64_t lo, int64_t rows) {
     rc = build_tmap(c);
     if (rc) return rc;
   }
-  if (rows)
-    KNB_CUDA(cudaMemcpyAsync(c->X_own + lo * c->d, host, sizeof(double) * rows * c->d, cudaMemcpyHostToDevice,
-                             c->stream));
+  if (rows) {  // (ordered after the stream's earlier work; synchronous)
+    KNB_CUDA(cudaStreamSynchronize(c->stream));
+    KNB_CUDA(staged_copy(c->device, c->X_own + lo * c->d, host, sizeof(double) * rows * c->d, true));
+  }
   return KNB_OK;
 }
 
@@ -1477,9 +1479,13 @@ int knb_get_assignments(knb_ctx* c, int32_t* out, int64_t lo, int64_t count) {
   if (!c || (!out && count > 0)) return fail(KNB_E_ARG, "null argument");
   if (lo < 0 || count < 0 || lo + count > c->n_local) return fail(KNB_E_ARG, "range outside the shard");
   KNB_CUDA(cudaSetDevice(c->device));
-  if (count)
-    KNB_CUDA(cudaMemcpyAsync(out, c->assign + lo, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream));
   KNB_CUDA(cudaStreamSynchronize(c->stream));
+  if (count) KNB_CUDA(staged_copy(c->device, out, c->assign + lo, sizeof(int32_t) * count, false));
+  return KNB_OK;
+}
+
+int knb_staging_reserve(int device) {
+  KNB_CUDA(staging_reserve(device));
   return KNB_OK;
 }
 

@@ -193,6 +193,11 @@ size_t mti_tc_bimg_bytes(int k);
 cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, cudaStream_t s);
 cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s);
 
+// staged copies between pageable host memory and HBM (hostcopy.cu)
+constexpr size_t STAGE_MIN = 64ull << 20;  // smaller copies go straight through cudaMemcpy
+cudaError_t staged_copy(int device, void* dst, const void* src, size_t bytes, bool h2d);
+cudaError_t staging_reserve(int device);
+
 // deterministic cluster-sorted accumulation (segsum.cu)
 struct SegArgs {
   const void* X;         // f32 or f64 rows
