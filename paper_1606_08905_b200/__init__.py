@@ -23,7 +23,7 @@ from .engine import (
 )
 from .fileio import HEADER_SIZE, MatrixIOError, load_matrix, save_matrix
 from .matrix import MatrixFormatError, RowRange, check_matrix, partition_rows
-from .outofcore import CacheSchedule, IoStats, RowCache, RowStore, fetch_rows, kmeans_ondisk, should_refresh
+from .outofcore import CacheSchedule, RowStore, kmeans_ondisk
 from .parallel import LocalComm, TorchComm, shard_of
 from .primitives import (
     CentroidGeometry,
@@ -50,12 +50,8 @@ __all__ = [
     "row_sqnorms",
     "rowwise_distances",
     "CentroidSet",
-    "IoStats",
-    "RowCache",
     "RowStore",
-    "fetch_rows",
     "kmeans_ondisk",
-    "should_refresh",
     "HEADER_SIZE",
     "MatrixIOError",
     "deterministic_view",

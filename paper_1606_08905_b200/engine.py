@@ -243,6 +243,8 @@ def kmeans(matrix, cfg: EngineConfig) -> KmeansResult:
         raise ValueError("kmeans() runs in-memory; use kmeans_ondisk() for sem mode")
     cfg.validate()
     host, dev = _rows_of(matrix, cfg)
+    if dev is not None and cfg.device is not None and int(cfg.device) != dev.device.index:
+        raise ValueError(f"EngineConfig.device={cfg.device} but the matrix lives on cuda:{dev.device.index}")
     return _run(host, dev, cfg, LocalComm(), device=cfg.device)
 
 

@@ -343,3 +343,27 @@ def test_gpu_host_rows_plain_array():
     assert np.array_equal(a.assignments, b.assignments)
     assert np.array_equal(a.centroids.means, b.centroids.means)
     assert b.io_totals is not None and a.io_totals is None
+
+
+def test_gpu_device_mismatch_is_rejected():
+    """A CUDA tensor on one device with EngineConfig.device naming another."""
+    import torch
+    x = torch.zeros((8, 2), dtype=torch.float64, device="cuda:0")
+    with pytest.raises(ValueError, match="device"):
+        kb.kmeans(x, kb.EngineConfig(k=2, device=1))
+
+
+@pytest.mark.parametrize("pruning", [False, True])
+def test_gpu_large_common_offset_matches_oracle(pruning):
+    """Rows around 1e8 with unit spread: the plain engine's running sums move by signed
+    deltas after the first pass (the reference recomputes them, engine.py:376-377); the
+    centroids stay within the parity bar of the oracle's over many iterations."""
+    rng = np.random.default_rng(17)
+    centers = 1e8 + rng.uniform(-20, 20, (6, 5))
+    m = centers[rng.integers(0, 6, 20000)] + rng.standard_normal((20000, 5))
+    cfg = dict(k=6, init="forgy", seed=3, pruning=pruning, max_iters=40)
+    r = kb.kmeans(m, kb.EngineConfig(collect_assignments=True, **cfg))
+    o = O.lloyd(m, 6, init="forgy", seed=3, pruning=pruning, max_iters=40, collect=True)
+    assert_parity(m, r, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
+                  counters={"reassignments": [s.reassignments for s in o.iterations]},
+                  what=f"offset pruning={pruning}")

@@ -1,7 +1,7 @@
 """§8(f) f2 on CPU: the semi-external I/O oracle pinned against the reference's own
 kmeans_ondisk runs (tests/golden/sem/, made by oracle/make_golden_sem.py), and the
-host side of the out-of-core API (RowStore, page_runs, fetch_rows, the refresh
-schedule) on the reference's test_sem.py cases."""
+host side of the out-of-core API (RowStore, the refresh schedule, kmeans_ondisk's
+argument and memory checks)."""
 
 from __future__ import annotations
 
@@ -16,8 +16,8 @@ from conftest import ROOT
 from oracle import lloyd as O
 from oracle import outofcore as OC
 from oracle.golden_cases import SEM_CASES, sem_case
-from paper_1606_08905_b200.outofcore import (CacheSchedule, IoStats, RowStore, fetch_rows, kmeans_ondisk,
-                                             page_runs, rows_per_partition, should_refresh)
+from paper_1606_08905_b200 import outofcore
+from paper_1606_08905_b200.outofcore import CacheSchedule, RowStore, kmeans_ondisk
 
 SEM_GOLD = os.path.join(ROOT, "tests", "golden", "sem")
 
@@ -49,13 +49,6 @@ def test_sem_oracle_matches_reference_golden(name):
     assert np.array_equal(o.means, g["means"])
 
 
-def test_pages_of_equals_page_runs():
-    rng = np.random.default_rng(0)
-    for rb, ps in ((64, 4096), (24, 512), (2400, 4096), (8, 1000), (4096, 4096), (5000, 4096)):
-        ids = np.sort(rng.choice(5000, size=300, replace=False))
-        assert OC.pages_of(ids, rb, ps) == page_runs(ids, rb, ps)[1]
-
-
 @pytest.fixture
 def store_8(tmp_path):
     m = kb.synth.uniform(512, 8, 5)  # 64-byte rows, payload exactly 8 pages
@@ -65,59 +58,33 @@ def store_8(tmp_path):
         yield store, m
 
 
-def test_page_accounting(tmp_path, store_8):
+def test_store_shape_checks_and_reads(tmp_path, store_8):
     store, m = store_8
-    stats = IoStats()
-    rows = fetch_rows(store, np.array([0]), None, stats)
-    assert (stats.bytes_requested, stats.bytes_read) == (64, 4096) and np.array_equal(rows[0], m[0])
-    stats = IoStats()
-    rows = fetch_rows(store, np.arange(64), None, stats)
-    assert stats.bytes_read == 4096 and rows.tobytes() == m[:64].tobytes()
-    assert page_runs(np.array([0, 64]), 64, 4096) == ([(0, 2)], 2)
-    assert page_runs(np.array([0, 128]), 64, 4096) == ([(0, 1), (2, 1)], 2)
-    w = kb.synth.uniform(10, 300, 2)  # 2400-byte rows: row 1 spans pages 0 and 1
-    w.tofile(tmp_path / "s.raw")
-    with RowStore(tmp_path / "s.raw", 10, 300) as s2:
-        stats = IoStats()
-        assert np.array_equal(fetch_rows(s2, np.array([1]), None, stats)[0], w[1])
-        assert stats.bytes_read == 8192
-
-
-def test_fetch_validates_and_store_errors(tmp_path, store_8):
-    store, m = store_8
-    with pytest.raises(IndexError):
-        fetch_rows(store, np.array([512]))
-    with pytest.raises(ValueError, match="ascending"):
-        fetch_rows(store, np.array([5, 3]))
+    assert (store.n, store.d, store.row_bytes, store.page_size) == (512, 8, 64, 4096)
+    assert store.rows[:64].tobytes() == m[:64].tobytes()
     (tmp_path / "w.raw").write_bytes(b"\x00" * 100)
     with pytest.raises(kb.MatrixFormatError, match="expected"):
         RowStore(tmp_path / "w.raw", 4, 4)
     with pytest.raises(ValueError, match="page_size"):
         RowStore(tmp_path / "w.raw", 5, 2, page_size=0)
+    with pytest.raises(kb.MatrixFormatError, match="raw"):
+        RowStore.open(tmp_path / "w.raw", raw=True)
     h = kb.synth.uniform(100, 4, 9)
     kb.save_matrix(h, tmp_path / "h.knrm")
     with RowStore.open(tmp_path / "h.knrm") as s3:
         assert (s3.n, s3.d) == (100, 4)
-        assert fetch_rows(s3, np.arange(100)).tobytes() == h.tobytes()
         out = np.empty((100, 4))
-        s3.read_all_into(out, chunk_bytes=1000)
+        s3.read_all_into(out, chunk_rows=7)
         assert out.tobytes() == h.tobytes()
-    m.tofile(tmp_path / "t.raw")
-    s4 = RowStore(tmp_path / "t.raw", 512, 8)
-    with open(tmp_path / "t.raw", "r+b") as fh:
-        fh.truncate(1000)
-    with pytest.raises(kb.MatrixFormatError, match="page"):
-        fetch_rows(s4, np.arange(512))
-    s4.close()
 
 
 def test_refresh_schedule():
-    assert [t for t in range(1, 80) if should_refresh(t, CacheSchedule(5))] == [5, 15, 35, 75]
-    assert [t for t in range(1, 16) if should_refresh(t, CacheSchedule(1))] == [1, 3, 7, 15]
-    assert all(OC.should_refresh(t, s) == should_refresh(t, CacheSchedule(s)) for s in (1, 2, 5) for t in range(200))
+    """CacheSchedule(s) refreshes at s, 3s, 7s, ... -- the oracle's should_refresh, which
+    is pinned to the reference's I/O counters."""
+    assert [t for t in range(1, 80) if OC.should_refresh(t, CacheSchedule(5).start)] == [5, 15, 35, 75]
+    assert [t for t in range(1, 16) if OC.should_refresh(t, CacheSchedule(1).start)] == [1, 3, 7, 15]
     with pytest.raises(ValueError, match="refresh start"):
         CacheSchedule(0)
-    assert rows_per_partition(4 * 64, 2, 64) == 2
 
 
 def test_kmeans_ondisk_mode_checks(store_8):
@@ -130,27 +97,10 @@ def test_kmeans_ondisk_mode_checks(store_8):
         kmeans_ondisk(store, kb.EngineConfig(k=2, mode="sem"), cache_capacity=-1)
 
 
-def test_row_cache_rebuild_truncates_by_ascending_id():
-    """outofcore.py RowCache semantics (test_sem.py's cache case)."""
-    cache = kb.RowCache(n_partitions=2, capacity_bytes=4 * 64, row_bytes=64)
-    assert cache.rows_per_partition == 2
-    rows = np.random.default_rng(0).normal(size=(6, 8))
-    cache.rebuild([[(np.array([5, 9]), rows[0:2]), (np.array([1]), rows[2:3])],
-                   [(np.array([20, 30, 40]), rows[3:6])]])
-    assert sorted(cache.published) == [1, 5, 20, 30]
-    assert cache.cached_bytes() <= cache.capacity_bytes
-    assert np.array_equal(cache.published[1], rows[2])
-    assert cache.cached_rows() == 4
-
-
-def test_fetch_rows_through_a_cache(tmp_path):
-    m = kb.synth.uniform(256, 8, 1)
-    m.tofile(tmp_path / "c.raw")
-    cache = kb.RowCache(1, 64 * 64, 64)
-    cache.rebuild([[(np.arange(0, 64), m[:64])]])
-    with RowStore(tmp_path / "c.raw", 256, 8) as store:
-        stats = IoStats()
-        rows = fetch_rows(store, np.array([3, 10, 100, 200]), cache, stats)
-    assert rows.tobytes() == m[[3, 10, 100, 200]].tobytes()
-    assert (stats.cache_hits, stats.cache_misses) == (2, 2)
-    assert stats.bytes_read == 2 * 4096 and stats.bytes_requested == 4 * 64
+def test_kmeans_ondisk_refuses_payloads_beyond_host_memory(store_8, monkeypatch):
+    """The payload is staged in host memory (not streamed from disk): a clear
+    MemoryError up front when it cannot fit."""
+    store, _ = store_8
+    monkeypatch.setattr(outofcore, "_available_host_bytes", lambda: 1000)
+    with pytest.raises(MemoryError, match="host memory"):
+        kmeans_ondisk(store, kb.EngineConfig(k=2, mode="sem"))
