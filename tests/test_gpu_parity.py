@@ -367,3 +367,5 @@ def test_gpu_large_common_offset_matches_oracle(pruning):
     assert_parity(m, r, o.means, o.assignments, o.n_iterations, want_prev=o.prev_means,
                   counters={"reassignments": [s.reassignments for s in o.iterations]},
                   what=f"offset pruning={pruning}")
+    # and in units of the spread, not of the 1e8 offset
+    assert float(np.abs(r.centroids.means - o.means).max()) < 1e-6
