@@ -290,25 +290,12 @@ def run_ours(args):
         torch.distributed.barrier()
     graph = None
     if not (world == 1 and not force_comm):
-        # capture one whole iteration -- local pass, NCCL all-reduce, finish -- as a CUDA
-        # graph on a side stream (the library enqueues on it via knb_set_stream)
+        # one whole iteration -- local pass, NCCL all-reduce, finish -- as a CUDA graph on
+        # a side stream (engine.capture_iteration: what kmeans_sharded replays)
         try:
-            g = torch.cuda.CUDAGraph()
-            side = torch.cuda.Stream()
-            side.wait_stream(stream)
-            with torch.cuda.stream(side):
-                run.ctx.set_stream(side.cuda_stream)
-                with torch.cuda.graph(g, stream=side):
-                    run.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-                    run.local()
-                    run.exchange()
-                    run.finish()
-            stream.wait_stream(side)
-            graph = g
+            graph = kb.engine.capture_iteration(run.ctx, comm, run.exch)
         except Exception as exc:  # pragma: no cover - eager fallback
             print(f"graph capture failed ({exc}); eager steps", file=sys.stderr)
-        finally:
-            run.ctx.set_stream(stream.cuda_stream or None)
         if world > 1:
             torch.distributed.barrier()
     torch.cuda.synchronize()

@@ -56,6 +56,9 @@ class TorchComm:
         self.world = dist.get_world_size(group)
         backend = dist.get_backend(group)
         self.cuda = backend == "nccl"
+        # NCCL collectives can be captured into a CUDA graph with the local pass and the
+        # finish (engine.capture_iteration); gloo's cannot
+        self.graph_capture = self.cuda
         self.scalar_device = device or ("cuda" if self.cuda else "cpu")
 
     def make_exchange(self, length: int, device: int | None):

@@ -47,3 +47,26 @@ def test_sharded_over_nccl_equals_single(nccl_group, init, pruning, f32):
     assert np.array_equal(a.assignments, b.assignments)
     assert np.array_equal(a.centroids.means, b.centroids.means)
     assert [s.wcss for s in a.iterations] == [s.wcss for s in b.iterations]
+
+
+@pytest.mark.parametrize("init,pruning,f32", [("forgy", True, False), ("kmeanspp", False, False),
+                                               ("forgy", False, True)])
+def test_sharded_graphed_loop_equals_single(nccl_group, init, pruning, f32):
+    """The multi-GPU loop without per-iteration host work: iteration 0 eagerly, then
+    replays of one captured iteration (local pass -> NCCL all-reduce -> finish) with the
+    stop flag on the device (engine._run_graphed; forced on the one-rank group)."""
+    d = 64 if f32 else 12
+    m = kb.synth.mixture(kb.synth.MixtureSpec(30000, d, 12, 6, "uniform", -3, 3, 0.8))
+    if f32:
+        m = m.astype(np.float32)
+    cfg = dict(k=12, init=init, seed=4, pruning=pruning, max_iters=40, batch=6)
+    a = kb.kmeans(m, kb.EngineConfig(**cfg))
+    nccl_group.force_graph = True
+    try:
+        b = kb.kmeans_sharded(m, kb.EngineConfig(**cfg), nccl_group, n_global=m.shape[0])
+    finally:
+        nccl_group.force_graph = False
+    assert a.n_iterations == b.n_iterations and a.converged == b.converged
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids.means, b.centroids.means)
+    assert [s.reassignments for s in a.iterations] == [s.reassignments for s in b.iterations]
