@@ -414,6 +414,27 @@ def run_ours(args):
         roof_k1["frac"] = roof_k1["achieved"] / roof_k1["peak"]
         roof_k1["hbm_GBps"] = bytes_ / k1_s / 1e9
         roof_k1["fp64_TFLOPs" if not tc else "tf32_TFLOPs"] = flops / k1_s / 1e12
+    # the reference's clause-2/3 candidate walk (mti_scan="exact": the reference's
+    # dist_comps / pruned_* counters) on the same rows, for the record (c2 / c3)
+    mti_exact = None
+    if world == 1 and cfg["pruning"] and name in ("c2", "c3"):
+        xcfg = kb.EngineConfig(k=k, init=cfg["init"], seed=seed, pruning=True, max_iters=args.warmup + 12,
+                               tolerance=cfg["tolerance"], device=local_rank, mti_scan="exact")
+        xr = kb.Lloyd(dev_rows, xcfg, ignore_stop=True)
+        for _ in range(args.warmup):
+            xr.step()
+        xe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        xe[0].record(stream)
+        for _ in range(10):
+            xr.step()
+        xe[1].record(stream)
+        torch.cuda.synchronize()
+        xs = [s for s in xr.ctx.stats() if s.t >= args.warmup]
+        mti_exact = {"ms_per_step": xe[0].elapsed_time(xe[1]) / 10, "steps": 10,
+                     "computed_fraction": sum(s.dist_comps for s in xs) / max(1, n * k * len(xs)),
+                     "note": "same run law, iterations after the warm-up; the reference's work counters"}
+        xr.close()
+        del xr
     tcinfo = run.ctx.tc_info() if tc else None
     run.close()
     del run  # (it holds the device rows; the e2e leg needs their HBM back)
@@ -468,7 +489,7 @@ def run_ours(args):
                    "l2": f"inputs {shard_bytes / 2**20:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
                    if shard_bytes > 126e6 else "inputs smaller than L2 (launch-bound config)",
                    "timed_iterations": f"{args.warmup}..{args.warmup + args.steps - 1} of one run"},
-        "roofline": roof, "roofline_k1": roof_k1, "cpu_baseline": base, "e2e": e2e,
+        "roofline": roof, "roofline_k1": roof_k1, "cpu_baseline": base, "e2e": e2e, "mti_exact": mti_exact,
         "gpu_launches": launches_per_step * args.steps, "clocks": clk,
         "setup": {"datagen_s": gen_s, "init_s": init_s, "dfma_peak_per_s": dfma_peak,
                   "copy_GBps_measured": mp["copy_bytes_per_s"] / 1e9, "kernels": desc},
