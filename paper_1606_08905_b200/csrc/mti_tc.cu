@@ -681,15 +681,22 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
 // The running-sum deltas of the rows the tcgen05 MTI pass moved (engine.py:345-353):
 // +x, +1, +||x||^2 to the new cluster, the same off the old one, from the pass's per-tile
 // records (a moved-row bit mask per row quarter, the old ids).  CTA b takes a contiguous
-// range of tiles; warp w walks groups of DG consecutive tiles (w, w + 8, ...) of it: the
-// group's moved rows are gathered 32 at a time (lane j loads row j, its old / new ids and
-// its exact-recipe ||x||^2 -- every load of the batch in flight at once) into a per-warp
-// staging area, then added in (tile, row) order to the warp's private sums (lanes 0-15 the
-// dims, lane 16 the counts, lane 17 ||x||^2).  The CTA adds its warps' sums in warp order
-// into partial b: deterministic for a fixed grid.
-constexpr int DG = 4;           // tiles per gathered group
+// range of tiles; warp w walks groups of DG = 8 consecutive tiles (w, w + DW, ... in the
+// range) and their moved rows in (tile, row) order, 32 at a time: lane j loads row j, its
+// old / new ids and its exact-recipe ||x||^2 -- the NEXT batch's loads are issued before
+// the current batch is added, so memory latency overlaps the additions -- and the warp
+// adds the staged batch in order to its private shared-memory sums (lanes 0-15 the dims,
+// lane 16 the counts, lane 17 ||x||^2; one uniform code path).  The CTA adds its warps'
+// sums in warp order into partial b: deterministic for a fixed grid.
+constexpr int DG = 8;           // tiles per group (32 mask words: one per lane)
 constexpr int DW = 8;           // warps per CTA
 constexpr int DST = XD + 1;     // staging row stride (doubles)
+
+struct DeltaBatch {
+  int n;                        // rows in the batch (warp-uniform), 0 = none
+  int to, from;                 // lane j: row j's new / old cluster
+  double x[XD];
+};
 
 __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArgs a) {
   pdl_enter();
@@ -702,84 +709,106 @@ __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArg
   double* cnt = acc + k * XD;
   double* sqa = cnt + k;
   double* stg = dsm + (size_t)DW * per + (size_t)warp * 32 * DST;
-  int* ent_to = reinterpret_cast<int*>(dsm + (size_t)DW * per + (size_t)DW * 32 * DST) + warp * 64;
-  int* ent_from = ent_to + 32;
+  int* ent = reinterpret_cast<int*>(dsm + (size_t)DW * per + (size_t)DW * 32 * DST) + warp * 64;
   for (int e = lane; e < per; e += 32) acc[e] = 0.0;
   __syncwarp();
   const long long T = (a.n + XT - 1) / XT;
   const long long lo = T * blockIdx.x / gridDim.x, hi = T * (blockIdx.x + 1) / gridDim.x;
-  for (long long g0 = lo + (long long)warp * DG; g0 < hi; g0 += (long long)DW * DG) {
-    const int ng = (int)min((long long)DG, hi - g0);
-    // mask word w (tile g0 + w / 4, quarter w % 4) in lane w, and the exclusive prefix count
-    unsigned mw = 0;
-    if (lane < 4 * ng) mw = reinterpret_cast<const unsigned*>(a.recs + (size_t)(g0 + (lane >> 2)) * TC_REC)[lane & 3];
-    int c = __popc(mw), pre = c;
+
+  // cursor over this warp's moved rows: the current group, its masks, the rows taken
+  long long g0 = lo + (long long)warp * DG;
+  unsigned mw = 0;
+  int pre = 0, cw = 0, total = 0, taken = 0;
+  auto load_group = [&]() {
+    mw = 0;
+    if (g0 < hi) {
+      const long long t = g0 + (lane >> 2);
+      if (t < hi) mw = reinterpret_cast<const unsigned*>(a.recs + (size_t)t * TC_REC)[lane & 3];
+    }
+    cw = __popc(mw);
+    int x = cw;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += v;
+      const int v = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += v;
     }
-    const int total = __shfl_sync(0xffffffffu, pre, 31);
-    pre -= c;
-    for (int b0 = 0; b0 < total; b0 += 32) {
-      // lane j: moved row b0 + j of the group
-      const int J = b0 + lane;
-      int wsel = -1;
-      for (int w = 0; w < 4 * ng; ++w) {
-        const int pw = __shfl_sync(0xffffffffu, pre, w), cw = __shfl_sync(0xffffffffu, c, w);
-        if (J >= pw && J < pw + cw) wsel = w;
-      }
-      int to = 0, from = 0;
-      long long row = -1;
-      double x[XD];
-      double sq = 0.0;
-      const unsigned mws = __shfl_sync(0xffffffffu, mw, wsel < 0 ? 0 : wsel);
-      const int pws = __shfl_sync(0xffffffffu, pre, wsel < 0 ? 0 : wsel);
-      if (wsel >= 0) {
-        const int bit = __fns(mws, 0, J - pws + 1);
-        const long long t = g0 + (wsel >> 2);
-        const int r = (wsel & 3) * 32 + bit;
-        row = t * XT + r;
-        from = a.recs[(size_t)t * TC_REC + 16 + r];
-        to = a.assign[row];
-        const double2* xr = reinterpret_cast<const double2*>(a.X + row * XD);
-#pragma unroll
-        for (int q = 0; q < XD / 2; ++q) {
-          const double2 v = __ldg(xr + q);
-          x[2 * q] = v.x;
-          x[2 * q + 1] = v.y;
-        }
-        sq = exact_sq_fixed<XD>(x, Zero{});
-#pragma unroll
-        for (int e = 0; e < XD; ++e) stg[lane * DST + e] = x[e];
-        stg[lane * DST + XD] = sq;
-      }
-      ent_to[lane] = to;
-      ent_from[lane] = from;
-      __syncwarp();
-      const int nb = min(32, total - b0);
-      for (int j = 0; j < nb; ++j) {
-        const int t = ent_to[j], f = ent_from[j];
-        if (lane < XD) {
-          const double xv = stg[j * DST + lane];
-          double* pt = acc + t * XD + lane;
-          double* pf = acc + f * XD + lane;
-          const double vt = *pt, vf = *pf;
-          *pt = vt + xv;
-          *pf = vf - xv;
-        } else if (lane == XD) {
-          const double vt = cnt[t], vf = cnt[f];
-          cnt[t] = vt + 1.0;
-          cnt[f] = vf - 1.0;
-        } else if (lane == XD + 1) {
-          const double q = stg[j * DST + XD];
-          const double vt = sqa[t], vf = sqa[f];
-          sqa[t] = vt + q;
-          sqa[f] = vf - q;
-        }
-      }
-      __syncwarp();
+    total = __shfl_sync(0xffffffffu, x, 31);
+    pre = x - cw;
+    taken = 0;
+  };
+  // the next batch: ids from the masks, then its loads issued (not waited on)
+  auto next = [&](DeltaBatch& bt) {
+    bt.n = 0;
+    while (taken >= total) {  // the current group is used up (or empty): the warp's next one
+      g0 += (long long)DW * DG;
+      if (g0 >= hi) return;
+      load_group();
     }
+    bt.n = min(32, total - taken);
+    const int J = taken + lane;
+    taken += bt.n;
+    // word holding moved row J: the last word whose prefix <= J (binary search on lanes)
+    int w = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      const int pw = __shfl_sync(0xffffffffu, pre, w + step);
+      if (pw <= J) w += step;
+    }
+    const unsigned mws = __shfl_sync(0xffffffffu, mw, w);
+    const int pws = __shfl_sync(0xffffffffu, pre, w);
+    bt.to = 0;
+    bt.from = 0;
+    if (lane < bt.n) {
+      const int bit = __fns(mws, 0, J - pws + 1);
+      const long long t = g0 + (w >> 2);
+      const int r = (w & 3) * 32 + bit;
+      const long long row = t * XT + r;
+      bt.from = a.recs[(size_t)t * TC_REC + 16 + r];
+      bt.to = a.assign[row];
+      const double2* xr = reinterpret_cast<const double2*>(a.X + row * XD);
+#pragma unroll
+      for (int q = 0; q < XD / 2; ++q) {
+        const double2 v = __ldg(xr + q);
+        bt.x[2 * q] = v.x;
+        bt.x[2 * q + 1] = v.y;
+      }
+    }
+  };
+  DeltaBatch cur, nxt;
+  load_group();
+  next(cur);
+  while (cur.n > 0) {
+    // stage the current batch (its loads complete here)
+    if (lane < cur.n) {
+      const double sq = exact_sq_fixed<XD>(cur.x, Zero{});
+#pragma unroll
+      for (int e = 0; e < XD; ++e) stg[lane * DST + e] = cur.x[e];
+      stg[lane * DST + XD] = sq;
+    }
+    reinterpret_cast<int2*>(ent)[lane] = make_int2(cur.to, cur.from);
+    const int nb = cur.n;
+    next(nxt);  // the following batch's loads are in flight during the additions
+    __syncwarp();
+    // per lane: the sum it owns is base[cluster * stride] (dims: acc[c][e]; lane 16: cnt[c];
+    // lane 17: sqa[c]) and the value it adds is stg[row][voff] (lane 16: 1)
+    const bool act = lane < XD + 2;
+    double* base = lane < XD ? acc + lane : (lane == XD ? cnt : sqa);
+    const int stride = lane < XD ? XD : 1;
+    const int voff = lane < XD ? lane : XD;
+    const bool one = lane == XD;
+    for (int j = 0; j < nb; ++j) {
+      const int2 tf = reinterpret_cast<const int2*>(ent)[j];
+      double* p1 = base + tf.x * stride;
+      double* p2 = base + tf.y * stride;
+      const double v = one ? 1.0 : stg[j * DST + voff];
+      if (act) {
+        const double v1 = *p1, v2 = *p2;
+        *p1 = v1 + v;
+        *p2 = v2 - v;
+      }
+    }
+    __syncwarp();
+    cur = nxt;
   }
   __syncthreads();
   double* out = a.partials + (long long)blockIdx.x * acc_len(k, XD);
