@@ -177,7 +177,7 @@ int knb_get_stats(knb_ctx* ctx, knb_iter_stats* out, int32_t max_count, int32_t*
 int knb_get_state(knb_ctx* ctx, int32_t* stop, int32_t* converged, int64_t* t, int32_t* count_error);
 int knb_get_centroids(knb_ctx* ctx, double* means, double* prev_means, int64_t* counts, double* drift);
 int knb_get_assignments(knb_ctx* ctx, int32_t* out, int64_t lo, int64_t count);
-/* Host transfers of 64 MB or more between pageable caller memory and HBM (the rows of
+/* Host transfers of 16 MB or more between pageable caller memory and HBM (the rows of
  * knb_upload_rows / _f32, the assignments of knb_get_assignments) are staged through a
  * pool of pinned chunks by eight threads, overlapping CPU copies with DMA.  The pool is
  * allocated on first use; knb_staging_reserve allocates it ahead of a timed call. */

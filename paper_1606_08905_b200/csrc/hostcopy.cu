@@ -8,7 +8,7 @@
 // so CPU copying and DMA overlap and the copy is bound by the host link instead.  The
 // pinned pool (W x 2 chunks) is allocated once per device and reused by every later
 // copy (pinning memory is slow: ~1.4 GB/s).  Used by knb_upload_rows(_f32) and
-// knb_get_assignments for transfers of STAGE_MIN bytes or more.
+// knb_get_assignments for transfers of STAGE_MIN (16 MB) bytes or more, in 8 MB chunks.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,7 +26,7 @@ namespace knb {
 
 namespace {
 
-constexpr size_t CHUNK = 32ull << 20;  // bytes per pinned chunk
+constexpr size_t CHUNK = 8ull << 20;  // bytes per pinned chunk
 constexpr int WORKERS = 8;
 
 struct Pool {

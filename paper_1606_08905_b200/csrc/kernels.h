@@ -194,7 +194,7 @@ cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, cudaStrea
 cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s);
 
 // staged copies between pageable host memory and HBM (hostcopy.cu)
-constexpr size_t STAGE_MIN = 64ull << 20;  // smaller copies go straight through cudaMemcpy
+constexpr size_t STAGE_MIN = 16ull << 20;  // smaller copies go straight through cudaMemcpy
 cudaError_t staged_copy(int device, void* dst, const void* src, size_t bytes, bool h2d);
 cudaError_t staging_reserve(int device);
 
