@@ -43,16 +43,19 @@
 //
 // Kernel shape (one CTA per SM, persistent over 128-row tiles, static schedule):
 //   warp 0      TMA producer: f64 row tiles (128 rows x 128 B, SWIZZLE_128B) through an
-//               NX-stage ring
-//   warp 1      TMEM allocation (2 x 128 columns: double-buffered accumulator) and the
-//               single-thread UMMA issuer
-//   warps 2-5   converters: one thread per row, f64 -> (x_hi, x_lo) TF32 operand tile
-//               (two 128-byte chunks) + the norm constants, NA-stage ring
-//   warps 6-9   epilogue: one thread per row (TMEM lane), key min trees, certificate,
-//               warp-wide exact rerank of uncertified rows, exact bound of the winner
-//               from the f64 tile, MTI state, moved rows accumulated in row order into
-//               warp-private sums (deterministic), then the f64 stage is released
-// HBM traffic per row: 128 B of rows + 12 B of state read + 9 B written (+4 if moved).
+//               NX-stage ring, tiles PF ahead prefetched into L2
+//   warp 1      TMEM allocation (NGRP x 128 columns: one accumulator per epilogue group)
+//               and the single-thread UMMA issuer
+//   warps 2-3   converters (NCONV): f64 -> (x_hi, x_lo) TF32 operand tile (two 128-byte
+//               chunks) + the norm constants + E(x) per row, NA-stage ring
+//   NGRP groups of four epilogue warps, tile i on group i % NGRP: one thread per row
+//               (TMEM lane), key min trees, certificate, warp-wide exact rerank of
+//               uncertified rows, exact bound of the winner from the f64 tile, MTI
+//               state; then the f64 stage is released and the tile's moved rows are
+//               written as a 144-byte record (row mask + old ids)
+// mti_tc_delta_kernel turns the records into per-CTA signed deltas of sums / counts /
+// sq in row order (deterministic), summed by reduce_kernel like every other pass.
+// HBM traffic per row: 128 B of rows + 13 B of state read + 13 B written (+ records).
 #include <cuda.h>
 #include <math_constants.h>
 
