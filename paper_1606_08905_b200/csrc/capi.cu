@@ -101,6 +101,9 @@ struct knb_ctx {
   void* tcx_bimg = nullptr;        // B operand image
   unsigned char* tcx_recs = nullptr;  // per-tile moved-row records (mti_tc_delta_kernel)
   unsigned long long* tcx_counters = nullptr;
+  long long* tcx_rq = nullptr;     // uncertified-row queue ({row, old id} pairs) and its count
+  unsigned long long* tcx_rq_count = nullptr;
+  long long tcx_rq_cap = 0;
 
   int DP = 0, DPm = 0, half_in_smem = 0;
   int G_dense = 1, G_mti = 1, G_mti_mma = 1;
@@ -504,7 +507,7 @@ bool tcx_ready(const knb_ctx* c) {
 }
 
 int launch_tcx(knb_ctx* c, int gate, float* dbg) {
-  KNB_CUDA(launch_mti_tc_prep(c->means, c->k, c->tcx_bimg, c->stream));
+  KNB_CUDA(launch_mti_tc_prep(c->means, c->k, c->tcx_bimg, dbg ? nullptr : c->tcx_rq_count, c->stream));
   MtiTcArgs t;
   t.X = c->X;
   t.n = c->n_local;
@@ -526,8 +529,14 @@ int launch_tcx(knb_ctx* c, int gate, float* dbg) {
   t.counters = c->tcx_counters;
   t.kmask = 0xFFFFFF80u;
   t.recs = c->tcx_recs;
+  t.rq = c->tcx_rq;
+  t.rq_count = c->tcx_rq_count;
+  t.rq_cap = c->tcx_rq_cap;
   KNB_CUDA(launch_mti_tc(&c->tmX128, t, c->G_dense, c->stream));
-  if (!dbg) KNB_CUDA(launch_mti_tc_delta(t, c->G_dense, c->stream));
+  if (!dbg) {
+    KNB_CUDA(launch_mti_tc_rerank(t, 2 * c->sms, c->stream));  // (two 8-warp CTAs per SM)
+    KNB_CUDA(launch_mti_tc_delta(t, c->G_dense, c->stream));
+  }
   return KNB_OK;
 }
 
@@ -825,6 +834,12 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
     const size_t rec_bytes = (size_t)((nl + 127) / 128) * TC_REC;
     if ((rc = dev_alloc(c, &recs, (rec_bytes + 7) / 8))) return bail(rc);
     c->tcx_recs = reinterpret_cast<unsigned char*>(recs);
+    // the rerank queue: 1/128 of the rows (c4 flags ~0.3% per pass), at least 64K entries
+    c->tcx_rq_cap = nl / 128 > 65536 ? nl / 128 : 65536;
+    double* rq = nullptr;
+    if ((rc = dev_alloc(c, &rq, (size_t)c->tcx_rq_cap * 2))) return bail(rc);
+    c->tcx_rq = reinterpret_cast<long long*>(rq);
+    if ((rc = dev_alloc(c, &c->tcx_rq_count, 1))) return bail(rc);
   }
   if ((rc = dev_alloc(c, &c->run, c->L))) return bail(rc);
   if ((rc = dev_alloc(c, &c->means, kd))) return bail(rc);
@@ -857,7 +872,7 @@ int knb_destroy(knb_ctx* c) {
   void* ptrs[] = {c->X_own, c->assign, c->upper, c->tight, c->means, c->prev, c->stage, c->drift, c->counts,
                   c->chn, c->cn2, c->half, c->half_min, c->wterm, c->run, c->partials, c->ctrl, c->fin_sync, c->stats,
                   c->bad, c->ids_dev, c->d2, c->kpp_bs, c->kpp_scalar, c->kpp_idx, c->X32_own, c->c32,
-                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->tcx_bimg, c->tcx_recs, c->tcx_counters, c->seg.counts,
+                  c->chn32, c->xn2, c->old_assign, c->tc_bound, c->tc_scratch, c->tc_fullq, c->tcq, c->tcq_count, c->tc_counters, c->tcx_bimg, c->tcx_recs, c->tcx_counters, c->tcx_rq, c->tcx_rq_count, c->seg.counts,
                   c->seg.lrank, c->seg.ctot, c->seg.cstart, c->seg.istart, c->seg.sorted, c->seg.records,
                   c->semA.fetched, c->semA.cslot, c->semA.crow, c->semA.cache, c->semA.bcount, c->semA.bpre,
                   c->semA.plo, c->semA.io};

@@ -184,13 +184,17 @@ struct MtiTcArgs {
   unsigned long long* counters;  // [0] uncertified (re-ranked) rows, cumulative
   uint32_t kmask;        // 0xFFFFFF80 (key mask, passed at run time)
   unsigned char* recs;   // per 128-row tile: moved-row masks (4 x u32) + old ids (u8 x 128)
+  long long* rq;         // uncertified rows queued for mti_tc_rerank_kernel: {row, old id} pairs
+  unsigned long long* rq_count;  // entries claimed this pass (zeroed by the prep kernel)
+  long long rq_cap;      // queue capacity (rows beyond it are re-ranked inside the pass)
 };
 constexpr int TC_REC = 16 + 128;
 cudaError_t launch_mti_tc_delta(const MtiTcArgs& a, int grid, cudaStream_t s);
 int mti_tc_stages(int d, int k);
 int mti_tc_prof(unsigned long long* out);  // 16 counters; returns 1 in a -DKNB_TCX_PROF=1 build
 size_t mti_tc_bimg_bytes(int k);
-cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, cudaStream_t s);
+cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, unsigned long long* rq_count, cudaStream_t s);
+cudaError_t launch_mti_tc_rerank(const MtiTcArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s);
 
 // staged copies between pageable host memory and HBM (hostcopy.cu)

@@ -85,7 +85,20 @@ constexpr uint32_t A_TILE = A_CHUNK + A_CONST;
 #define KNB_TCX_PF 6
 #endif
 constexpr int PF = KNB_TCX_PF;                 // tiles pulled into L2 ahead of their TMA load
-constexpr int NA = 2;                          // operand stages
+#ifndef KNB_TCX_NA
+#define KNB_TCX_NA 2
+#endif
+constexpr int NA = KNB_TCX_NA;                 // operand stages
+// ablations for timing studies only (wrong results): the converters skip the operand
+// writes / the epilogue stops after the key trees
+#ifndef KNB_TCX_ABL
+#define KNB_TCX_ABL 0
+#endif
+
+#ifndef KNB_TCX_NXMAX
+#define KNB_TCX_NXMAX 6
+#endif
+constexpr int NE = 8;                          // E(x) ring (tiles), indexed by tile & 7
 constexpr int TCOLS = 128;                     // TMEM columns per accumulator buffer
 #ifndef KNB_TCX_GROUPS
 #define KNB_TCX_GROUPS 3
@@ -107,6 +120,13 @@ constexpr int NCONV = KNB_TCX_CONV;            // converter warps (128 / (32 NCO
 constexpr int W_CONV = 2, W_EPI = 2 + NCONV;
 constexpr int THREADS = 32 * (W_EPI + 4 * NGRP);
 constexpr int TALLOC = NGRP <= 2 ? 2 * TCOLS : 4 * TCOLS;  // power-of-two TMEM allocation
+// TMEM accumulator buffers: tile i uses buffer i % NACC (any group).  With three groups the
+// four-buffer allocation holds a spare accumulator, so the in-order MMA issue runs one
+// tile further ahead of the slowest group
+#ifndef KNB_TCX_NACC
+#define KNB_TCX_NACC (TALLOC / TCOLS)
+#endif
+constexpr int NACC = KNB_TCX_NACC;
 
 __host__ __device__ inline uint32_t al(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -121,9 +141,9 @@ struct TcxSmem {
     b0 = o;   o += 2u * N * 128u;
     crow = o; o += (uint32_t)k * crow_stride<XD>() * 8u;
     hd = o;   o += (uint32_t)k * 16u;
-    ebuf = o; o += (uint32_t)nx * XT * 4u;
+    ebuf = o; o += (uint32_t)NE * XT * 4u;
     o = al(o, 16);
-    bars = o; o += 8 * (2 * nx + 2 * NA + 2 * NGRP) + 16;
+    bars = o; o += 8 * (2 * nx + 2 * NA + 2 * 4) + 16;
     total = o + 1024;  // runtime 1024-byte alignment of the dynamic window
   }
 };
@@ -145,11 +165,6 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[16]) {
                  : "r"(taddr)
                  : "memory");
   }
-}
-
-// fire-and-forget f64 add at a global address (L2 atomic unit, round to nearest)
-__device__ __forceinline__ void red_add_f64(double* p, double v) {
-  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 // K-major no-swizzle operand (8-row x 16-byte core matrices): byte offset of 16-byte
@@ -290,11 +305,11 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
   uint64_t* a_full = bars + 2 * NX;
   uint64_t* a_empty = a_full + NA;
   uint64_t* t_full = a_empty + NA;
-  uint64_t* t_empty = t_full + NGRP;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + NGRP);
+  uint64_t* t_empty = t_full + NACC;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(t_empty + NACC);
   double* crow = reinterpret_cast<double*>(sm + L.crow);
   double2* hd = reinterpret_cast<double2*>(sm + L.hd);
-  float* ebuf = reinterpret_cast<float*>(sm + L.ebuf);  // per stage: the rows' certificate bound E
+  float* ebuf = reinterpret_cast<float*>(sm + L.ebuf);  // per tile (& 7): the rows' certificate bound E
   const bool work = (int)blockIdx.x < a.gtc;  // extra CTAs (grid shared with other kernels) only write zeros
 
   // ---- setup: B operand image, exact-recipe centroid copy, {drift, half_min}, sums
@@ -319,7 +334,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       mbar_init(a_full + s, NCONV);
       mbar_init(a_empty + s, 1);
     }
-    for (int b = 0; b < NGRP; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(t_full + b, 1);
       mbar_init(t_empty + b, 4);
     }
@@ -339,7 +354,8 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
   const int mine = ntiles > t0 ? (ntiles - t0 + tstep - 1) / tstep : 0;  // tiles of this CTA
 
   // epilogue-side counters (reduced at the end)
-  long long reassigned = 0, skips = 0, computed = 0, flagged = 0;
+  // (32-bit: per thread at most tiles x k; reassignments are counted by mti_tc_delta_kernel)
+  unsigned skips = 0, computed = 0, flagged = 0;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -367,8 +383,8 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       pc.start();
       int b = 0, bph = 0;  // accumulator buffer of tile i (= its epilogue group) and its phase
       for (int i = 0; i < mine; ++i) {
-        const int sa = i & 1;  // NA == 2
-        mbar_sleep(a_full + sa, (i >> 1) & 1);
+        const int sa = i % NA;
+        mbar_sleep(a_full + sa, (i / NA) & 1);
         pc.lap(0);
         mbar_sleep(t_empty + b, bph ^ 1);
         pc.lap(1);
@@ -389,7 +405,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
         umma_commit(a_empty + sa);
         umma_commit(t_full + b);
         pc.lap(2);
-        if (++b == NGRP) { b = 0; bph ^= 1; }
+        if (++b == NACC) { b = 0; bph ^= 1; }
       }
       pc.flush(2, 3, true);
     }
@@ -402,16 +418,16 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
     pc.start();
     int s = 0, ph = 0;
     for (int i = 0; i < mine; ++i) {
-      const int sa = i & 1;
+      const int sa = i % NA;
       mbar_sleep(x_full + s, ph);
       pc.lap(0);
-      mbar_sleep(a_empty + sa, ((i >> 1) & 1) ^ 1);
+      mbar_sleep(a_empty + sa, ((i / NA) & 1) ^ 1);
       pc.lap(1);
       const unsigned char* xs = sm + L.x0 + s * X_TILE;
       unsigned char* A0 = sm + L.a0 + sa * A_TILE;
       unsigned char* AC = A0 + A_CHUNK;
 #pragma unroll
-      for (int rr = 0; rr < 4 / NCONV; ++rr) {
+      for (int rr = 0; rr < ((KNB_TCX_ABL & 1) ? 0 : 4 / NCONV); ++rr) {
       const int r = r0 + rr * 32 * NCONV;
       float hi[XD], lo[XD];
       float n0 = 0.0f, n1 = 0.0f;
@@ -439,7 +455,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       // the certificate's bound E(x) for the epilogue (f32 with a relative margin;
       // xn2 carries < 2^-20 relative error)
       const float xnb = xn2 * (1.0f + 0x1p-12f);
-      ebuf[s * XT + r] = (0x1p-20f * (12.5f * sqrtf(xnb) * cmaxf + 4.0f * (xnb + cmax2f)) +
+      ebuf[(i & (NE - 1)) * XT + r] = (0x1p-20f * (12.5f * sqrtf(xnb) * cmaxf + 4.0f * (xnb + cmax2f)) +
                           (8.0f * XD + 32.0f) * 0x1p-53f * (xnb + cmax2f)) * (1.0f + 0x1p-10f);
       }
       fence_proxy_async();
@@ -457,8 +473,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
     const int grp = (warp - W_EPI) >> 2;
     const int q = warp & 3;          // TMEM lane quarter
     const int r = q * 32 + lane;     // row within the tile
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(grp * TCOLS);
-    int tph = 0;  // phase of this group's accumulator buffer
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     auto state = [&](int i, int& av, double& uv) {
       const long long row = (long long)(t0 + i * tstep) * XT + r;
       const bool ok = i < mine && row < a.n;
@@ -482,6 +497,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       const double u = u0 + dh.x;                 // inflate (u + 0.0 == u)
       const bool skip = valid && u <= dh.y;       // clause 1
       const bool live = a.dbg ? valid : (valid && !skip);
+      double x[XD];
       if (!a.dbg) {
         skips += skip ? 1 : 0;
         if (skip && dh.x != 0.0) {  // the inflated bound is the skipped row's state
@@ -490,8 +506,9 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
         }
       }
       pc.lap(5);
-      mbar_sleep(t_full + grp, (uint32_t)tph);
-      tph ^= 1;
+      const int tb = i % NACC;  // the tile's accumulator buffer
+      const uint32_t tl = tq + (uint32_t)(tb * TCOLS);
+      mbar_sleep(t_full + tb, (uint32_t)((i / NACC) & 1));
       pc.lap(0);
       tc_fence_after();
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
@@ -551,37 +568,57 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(t_empty + grp);
+      if (lane == 0) mbar_arrive(t_empty + tb);
       pc.lap(1);
 
-      // the f64 rows of this tile (landed before the converters ran; the wait only
-      // orders this warp's reads after the TMA)
-      mbar_sleep(x_full + s, (uint32_t)ph);
       pc.lap(2);
-      const unsigned char* xs = sm + L.x0 + s * X_TILE;
       unsigned mm = 0;
       int win = k1 & 127;
-      double x[XD];
-      if (!a.dbg && lmask) {
-#pragma unroll
-        for (int c = 0; c < XD / 2; ++c) {
-          const double2 vv = *reinterpret_cast<const double2*>(xs + swz(r, c));
-          x[2 * c] = vv.x;
-          x[2 * c + 1] = vv.y;
-        }
+      if (!a.dbg && lmask && !(KNB_TCX_ABL & 2)) {
         bool cert = false;
         if (live) {
-          const float E = ebuf[s * XT + r];
+          const float E = ebuf[(i & (NE - 1)) * XT + r];
           const float m1 = __int_as_float(k1 & ~127), m2 = __int_as_float(k2 & ~127);
           // key slack (< 2^-16 relative each) and the f32 rounding of this test
           cert = (m2 - m1) > 2.0f * E + 0x1p-15f * (fabsf(m1) + fabsf(m2)) && win < k;
+          if (KNB_TCX_ABL & 16) cert = true;
+        }
+        {
+          // the f64 rows of this tile from the stage (landed before the converters ran; the
+          // wait only orders this warp's reads after the TMA)
+          mbar_sleep(x_full + s, (uint32_t)ph);
+          const unsigned char* xs = sm + L.x0 + s * X_TILE;
+          if (live) {
+#pragma unroll
+            for (int c = 0; c < XD / 2; ++c) {
+              const double2 vv = *reinterpret_cast<const double2*>(xs + swz(r, c));
+              x[2 * c] = vv.x;
+              x[2 * c + 1] = vv.y;
+            }
+          }
         }
         double nd = 0.0;
-        // uncertified rows: the whole warp re-ranks each one with the exact recipe,
-        // scan_block's order -- the current centroid first, then ascending ids, switch
-        // on strict < of the sqrt'ed distances (pruning.py:174-203)
+        // uncertified rows go to the rerank queue (mti_tc_rerank_kernel re-ranks them after
+        // the pass: a warp stalled on one row's k exact distances here would hold up the
+        // tile pipeline); beyond the queue's capacity the whole warp re-ranks each one here
+        // with the exact recipe, scan_block's order -- the current centroid first, then
+        // ascending ids, switch on strict < of the sqrt'ed distances (pruning.py:174-203)
         unsigned fl = __ballot_sync(0xffffffffu, live && !cert);
-        if (lane == 0) flagged += __popc(fl);
+        bool queued = false;
+        if (fl) {
+          if (lane == 0) flagged += __popc(fl);
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(a.rq_count, (unsigned long long)__popc(fl));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if ((fl >> lane) & 1u) {
+            const unsigned long long slot = base + __popc(fl & ((1u << lane) - 1u));
+            if (slot < (unsigned long long)a.rq_cap) {
+              reinterpret_cast<longlong2*>(a.rq)[slot] = make_longlong2(row, (long long)orig);
+              queued = true;
+            }
+          }
+          fl = __ballot_sync(0xffffffffu, (live && !cert) && !queued);
+        }
         while (fl) {
           const int f = __ffs(fl) - 1;
           fl &= fl - 1;
@@ -610,21 +647,18 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
             nd = bd;
           }
         }
-        if (live && cert) {
+        if (live && cert && !(KNB_TCX_ABL & 4)) {
           double cw[XD];
           load_crow<XD>(crow, win, cw);
           nd = sqrt(exact_sq_fixed<XD>(x, cw));
         }
-        const bool moved = live && win != orig;
-        if (live) {
+        const bool moved = live && !queued && win != orig;
+        if (live && !queued && !(KNB_TCX_ABL & 8)) {
           a.upper[row] = nd;
           a.tight[row] = 1;
-          if (moved) {
-            a.assign[row] = win;
-            ++reassigned;
-          }
+          if (moved) a.assign[row] = win;
         }
-        if (lane == 0) computed += (long long)__popc(lmask) * k;
+        if (lane == 0) computed += (unsigned)(__popc(lmask) * k);
         mm = __ballot_sync(0xffffffffu, moved);
       }
       // the stage goes back to the producer; the tile's moved rows go to global memory
@@ -657,8 +691,8 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
   const int kk = k * (XD + 2);
   __shared__ long long red[4 * NGRP][4];
   if (warp >= W_EPI) {
-    const long long c0 = warp_sum_ll(reassigned), c1 = warp_sum_ll(skips), c2 = warp_sum_ll(computed),
-                    c3 = warp_sum_ll(flagged);
+    const long long c0 = 0, c1 = warp_sum_ll((long long)skips), c2 = warp_sum_ll((long long)computed),
+                    c3 = warp_sum_ll((long long)flagged);
     if (lane == 0) {
       red[warp - W_EPI][0] = c0;
       red[warp - W_EPI][1] = c1;
@@ -674,7 +708,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
         for (int c = 0; c < 4; ++c) tot[c] += red[w][c];
     double* sc = out + kk;
     for (int c = 0; c < NSCAL; ++c) sc[c] = 0.0;
-    sc[S_REASSIGNED] = (double)tot[0];
+    sc[S_REASSIGNED] = 0.0;  // (mti_tc_delta_kernel counts the moved rows from the records)
     sc[S_SKIPS] = (double)tot[1];
     sc[S_COMPUTED] = (double)tot[2];
     if (a.counters && tot[3]) atomicAdd(a.counters, (unsigned long long)tot[3]);
@@ -684,22 +718,32 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
 // The running-sum deltas of the rows the tcgen05 MTI pass moved (engine.py:345-353):
 // +x, +1, +||x||^2 to the new cluster, the same off the old one, from the pass's per-tile
 // records (a moved-row bit mask per row quarter, the old ids).  CTA b takes a contiguous
-// range of tiles; warp w walks groups of DG = 8 consecutive tiles (w, w + DW, ... in the
-// range) and their moved rows in (tile, row) order, 32 at a time: lane j loads row j, its
-// old / new ids and its exact-recipe ||x||^2 -- the NEXT batch's loads are issued before
-// the current batch is added, so memory latency overlaps the additions -- and the warp
-// adds the staged batch in order to its private shared-memory sums (lanes 0-15 the dims,
-// lane 16 the counts, lane 17 ||x||^2; one uniform code path).  The CTA adds its warps'
-// sums in warp order into partial b: deterministic for a fixed grid.
-constexpr int DG = 8;           // tiles per group (32 mask words: one per lane)
+// range of tiles and walks it in chunks of dc tiles (256, or 128 when k is large): thread
+// t holds tile t's four mask words -- the next chunk's are loaded while the current one
+// is summed -- and an exclusive scan in shared memory makes the j-th moved row of the
+// chunk a binary search away; the moved rows are cut into batches of 32 and batch m goes
+// to warp m % DW.  A warp copies a batch into one of its two staging slots with cp.async
+// -- eight lanes per row, four rows per instruction (whole 128-byte lines, 16-byte chunks
+// swizzled by row so the per-row reads are conflict-free), plus each row's new id and the
+// word holding its old id -- and issues the NEXT batch's copies before it adds the current
+// one, in row order, to its private sums (lanes 0-15 the dims, lane 16 the counts, lane 17
+// ||x||^2, the row's exact-recipe sum of squares).  The CTA adds its warps' sums in warp
+// order into partial b: deterministic for a fixed grid.  The CTA also counts the moved
+// rows (the pass's reassignments).
 constexpr int DW = 8;           // warps per CTA
-constexpr int DST = XD + 1;     // staging row stride (doubles)
 
-struct DeltaBatch {
-  int n;                        // rows in the batch (warp-uniform), 0 = none
-  int to, from;                 // lane j: row j's new / old cluster
-  double x[XD];
-};
+__host__ __device__ inline int delta_chunk(int k) { return k <= 112 ? 256 : 128; }
+
+size_t delta_smem(int k) {
+  return (size_t)DW * k * (XD + 2) * sizeof(double)   // private sums
+         + (size_t)DW * 2 * 32 * XD * sizeof(double)  // staging rows
+         + (size_t)DW * 2 * 32 * sizeof(double)       // their ||x||^2
+         + (size_t)DW * 2 * 32 * sizeof(int2)         // new / old ids
+         + (size_t)8 * delta_chunk(k) * sizeof(unsigned);  // mask words + prefixes
+}
+
+// staging offset (doubles) of element e of row rr: 16-byte chunks swizzled by the row
+__device__ __forceinline__ int sw_off(int rr, int e) { return rr * XD + ((((e >> 1) ^ rr) & 7) << 1) + (e & 1); }
 
 __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArgs a) {
   pdl_enter();
@@ -707,125 +751,292 @@ __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArg
   if (a.gate && a.ctrl->mti_choice != 1) return;
   extern __shared__ double dsm[];
   const int k = a.k, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int dc = delta_chunk(k);
   const int per = k * (XD + 2);
   double* acc = dsm + (size_t)warp * per;
   double* cnt = acc + k * XD;
   double* sqa = cnt + k;
-  double* stg = dsm + (size_t)DW * per + (size_t)warp * 32 * DST;
-  int* ent = reinterpret_cast<int*>(dsm + (size_t)DW * per + (size_t)DW * 32 * DST) + warp * 64;
+  double* stg = dsm + (size_t)DW * per + (size_t)warp * 2 * 32 * XD;            // [slot][row][16]
+  double* sqs = dsm + (size_t)DW * per + (size_t)DW * 2 * 32 * XD + warp * 64;  // [slot][row]
+  int2* ids = reinterpret_cast<int2*>(dsm + (size_t)DW * per + (size_t)DW * 2 * 32 * XD + DW * 64) + warp * 64;
+  unsigned* mwd = reinterpret_cast<unsigned*>(reinterpret_cast<int2*>(dsm + (size_t)DW * per +
+                                                                       (size_t)DW * 2 * 32 * XD + DW * 64) + DW * 64);
+  int* wpre = reinterpret_cast<int*>(mwd + 4 * dc);  // exclusive prefix of the words' popcounts
+  __shared__ int wtot[DW];
+  __shared__ double dummy[DW];  // the idle lanes' target
   for (int e = lane; e < per; e += 32) acc[e] = 0.0;
   __syncwarp();
   const long long T = (a.n + XT - 1) / XT;
   const long long lo = T * blockIdx.x / gridDim.x, hi = T * (blockIdx.x + 1) / gridDim.x;
+  long long moved = 0;
+  const uint32_t stg_s = smem_u32(stg), ids_s = smem_u32(ids);
+  auto masks = [&](long long c0) {  // tile c0 + tid's four words
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tid < dc && c0 + tid < hi) v = *reinterpret_cast<const uint4*>(a.recs + (size_t)(c0 + tid) * TC_REC);
+    return v;
+  };
+  uint4 mk = masks(lo);
 
-  // cursor over this warp's moved rows: the current group, its masks, the rows taken
-  long long g0 = lo + (long long)warp * DG;
-  unsigned mw = 0;
-  int pre = 0, cw = 0, total = 0, taken = 0;
-  auto load_group = [&]() {
-    mw = 0;
-    if (g0 < hi) {
-      const long long t = g0 + (lane >> 2);
-      if (t < hi) mw = reinterpret_cast<const unsigned*>(a.recs + (size_t)t * TC_REC)[lane & 3];
-    }
-    cw = __popc(mw);
-    int x = cw;
+  for (long long c0 = lo; c0 < hi; c0 += dc) {
+    const int run = __popc(mk.x) + __popc(mk.y) + __popc(mk.z) + __popc(mk.w);
+    if (tid < dc) reinterpret_cast<uint4*>(mwd)[tid] = mk;
+    int inc = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += v;
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
     }
-    total = __shfl_sync(0xffffffffu, x, 31);
-    pre = x - cw;
-    taken = 0;
-  };
-  // the next batch: ids from the masks, then its loads issued (not waited on)
-  auto next = [&](DeltaBatch& bt) {
-    bt.n = 0;
-    while (taken >= total) {  // the current group is used up (or empty): the warp's next one
-      g0 += (long long)DW * DG;
-      if (g0 >= hi) return;
-      load_group();
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    int wbase = 0, M = 0;
+    for (int w = 0; w < DW; ++w) {
+      wbase += w < warp ? wtot[w] : 0;
+      M += wtot[w];
     }
-    bt.n = min(32, total - taken);
-    const int J = taken + lane;
-    taken += bt.n;
-    // word holding moved row J: the last word whose prefix <= J (binary search on lanes)
-    int w = 0;
-#pragma unroll
-    for (int step = 16; step; step >>= 1) {
-      const int pw = __shfl_sync(0xffffffffu, pre, w + step);
-      if (pw <= J) w += step;
+    if (tid < dc) {
+      int p = wbase + inc - run;
+      wpre[4 * tid] = p;
+      p += __popc(mk.x);
+      wpre[4 * tid + 1] = p;
+      p += __popc(mk.y);
+      wpre[4 * tid + 2] = p;
+      p += __popc(mk.z);
+      wpre[4 * tid + 3] = p;
     }
-    const unsigned mws = __shfl_sync(0xffffffffu, mw, w);
-    const int pws = __shfl_sync(0xffffffffu, pre, w);
-    bt.to = 0;
-    bt.from = 0;
-    if (lane < bt.n) {
-      const int bit = __fns(mws, 0, J - pws + 1);
-      const long long t = g0 + (w >> 2);
-      const int r = (w & 3) * 32 + bit;
-      const long long row = t * XT + r;
-      bt.from = a.recs[(size_t)t * TC_REC + 16 + r];
-      bt.to = a.assign[row];
-      const double2* xr = reinterpret_cast<const double2*>(a.X + row * XD);
-#pragma unroll
-      for (int q = 0; q < XD / 2; ++q) {
-        const double2 v = __ldg(xr + q);
-        bt.x[2 * q] = v.x;
-        bt.x[2 * q + 1] = v.y;
+    __syncthreads();
+    moved += M;
+    mk = masks(c0 + dc);  // the next chunk's words, in flight during this one
+
+    // batch m of the chunk (its moved rows [32m, 32m + 32)) into staging slot sl; returns
+    // the batch's rows (0: none) and, in lane j, row j's old-id byte position.  Always
+    // commits one cp.async group.
+    auto fetch = [&](int m, int sl, int& sub) -> int {
+      const int n = 32 * m < M ? min(32, M - 32 * m) : 0;
+      long long row = 0;
+      if (lane < n) {
+        const int J = 32 * m + lane;
+        int w = 0;  // the last word whose prefix <= J
+        for (int step = 2 * dc; step; step >>= 1)
+          if (w + step < 4 * dc && wpre[w + step] <= J) w += step;
+        const int bit = __fns(mwd[w], 0, J - wpre[w] + 1);
+        const long long t = c0 + (w >> 2);
+        const int r = (w & 3) * 32 + bit;
+        row = t * XT + r;
+        sub = r & 3;
+        const uint32_t id = ids_s + (uint32_t)((sl * 32 + lane) * sizeof(int2));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(id), "l"(a.assign + row) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(id + 4),
+                     "l"(a.recs + (size_t)t * TC_REC + 16 + (r & ~3)) : "memory");
       }
-    }
-  };
-  DeltaBatch cur, nxt;
-  load_group();
-  next(cur);
-  while (cur.n > 0) {
-    // stage the current batch (its loads complete here)
-    if (lane < cur.n) {
-      const double sq = exact_sq_fixed<XD>(cur.x, Zero{});
+      // eight lanes per row: lane l copies 16-byte chunk l & 7 of row 4 i + l / 8
 #pragma unroll
-      for (int e = 0; e < XD; ++e) stg[lane * DST + e] = cur.x[e];
-      stg[lane * DST + XD] = sq;
-    }
-    reinterpret_cast<int2*>(ent)[lane] = make_int2(cur.to, cur.from);
-    const int nb = cur.n;
-    next(nxt);  // the following batch's loads are in flight during the additions
-    __syncwarp();
-    // per lane: the sum it owns is base[cluster * stride] (dims: acc[c][e]; lane 16: cnt[c];
-    // lane 17: sqa[c]) and the value it adds is stg[row][voff] (lane 16: 1)
-    const bool act = lane < XD + 2;
-    double* base = lane < XD ? acc + lane : (lane == XD ? cnt : sqa);
-    const int stride = lane < XD ? XD : 1;
-    const int voff = lane < XD ? lane : XD;
-    const bool one = lane == XD;
-    for (int j = 0; j < nb; ++j) {
-      const int2 tf = reinterpret_cast<const int2*>(ent)[j];
-      double* p1 = base + tf.x * stride;
-      double* p2 = base + tf.y * stride;
-      const double v = one ? 1.0 : stg[j * DST + voff];
-      if (act) {
-        const double v1 = *p1, v2 = *p2;
-        *p1 = v1 + v;
-        *p2 = v2 - v;
+      for (int i = 0; i < 8; ++i) {
+        const int rr = 4 * i + (lane >> 3);
+        const long long rw = __shfl_sync(0xffffffffu, row, rr);
+        if (rr < n)
+          cp_async16_s(stg_s + (uint32_t)((sl * 32 * XD + sw_off(rr, 2 * (lane & 7))) * sizeof(double)),
+                       a.X + rw * XD + 2 * (lane & 7));
       }
+      cp_async_commit();
+      return n;
+    };
+    int m = warp, sl = 0, sub = 0, nsub = 0;
+    int n = fetch(m, 0, sub);
+    while (n > 0) {
+      const int nn = fetch(m + DW, sl ^ 1, nsub);  // the next batch's copies are in flight during the additions
+      cp_async_wait_1();
+      __syncwarp();
+      const double* sg = stg + sl * 32 * XD;
+      double* sq = sqs + sl * 32;
+      int2* id = ids + sl * 32;
+      if (lane < n) {
+        double x[XD];
+#pragma unroll
+        for (int e = 0; e < XD; e += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(sg + sw_off(lane, e));
+          x[e] = v.x;
+          x[e + 1] = v.y;
+        }
+        sq[lane] = exact_sq_fixed<XD>(x, Zero{});
+        const int2 v = id[lane];
+        id[lane].y = (v.y >> (8 * sub)) & 0xFF;  // the old id's byte
+      }
+      __syncwarp();
+      // per lane: the sum it owns is base[cluster * stride] (dims: acc[c][e]; lane 16: cnt[c];
+      // lane 17: sqa[c]; lanes 18-31 a dummy slot) and the value it adds (lane 16: 1).  No
+      // branches: every lane runs the same read-modify-writes.  Two consecutive rows whose
+      // four clusters are distinct (the usual case) are read, added and written together;
+      // otherwise one after the other -- the same order of additions per sum either way.
+      double* base = lane < XD ? acc + lane : (lane == XD ? cnt : (lane == XD + 1 ? sqa : dummy + warp));
+      const int stride = lane < XD ? XD : (lane <= XD + 1 ? 1 : 0);
+      const int to_l = id[lane].x, fr_l = id[lane].y;
+      auto val = [&](int j) {
+        return lane < XD ? sg[sw_off(j, lane)] : (lane == XD + 1 ? sq[j] : 1.0);
+      };
+      int j = 0;
+      while (j < n) {
+        const int t0 = __shfl_sync(0xffffffffu, to_l, j), f0 = __shfl_sync(0xffffffffu, fr_l, j);
+        const int j1 = j + 1 < n ? j + 1 : j;
+        const int t1 = __shfl_sync(0xffffffffu, to_l, j1), f1 = __shfl_sync(0xffffffffu, fr_l, j1);
+        if (j + 1 < n && t1 != t0 && t1 != f0 && f1 != t0 && f1 != f0) {
+          const double v0 = val(j), w0 = val(j + 1);
+          double* a0 = base + t0 * stride;
+          double* b0 = base + f0 * stride;
+          double* a1 = base + t1 * stride;
+          double* b1 = base + f1 * stride;
+          const double ra0 = *a0, rb0 = *b0, ra1 = *a1, rb1 = *b1;
+          *a0 = ra0 + v0;
+          *b0 = rb0 - v0;
+          *a1 = ra1 + w0;
+          *b1 = rb1 - w0;
+          j += 2;
+        } else {
+          const double v0 = val(j);
+          double* a0 = base + t0 * stride;
+          double* b0 = base + f0 * stride;
+          const double ra0 = *a0, rb0 = *b0;
+          *a0 = ra0 + v0;
+          *b0 = rb0 - v0;
+          j += 1;
+        }
+      }
+      __syncwarp();
+      n = nn;
+      sub = nsub;
+      m += DW;
+      sl ^= 1;
     }
-    __syncwarp();
-    cur = nxt;
+    cp_async_wait_all();
+    __syncthreads();  // (the next chunk overwrites the words and prefixes)
   }
-  __syncthreads();
   double* out = a.partials + (long long)blockIdx.x * acc_len(k, XD);
   for (int e = tid; e < per; e += DW * 32) {
     double v = 0.0;
     for (int w = 0; w < DW; ++w) v += dsm[(size_t)w * per + e];
     out[e] = v;
   }
+  if (tid == 0) out[per + S_REASSIGNED] = (double)moved;
+}
+
+// The uncertified rows of the pass (the queue the epilogue filled), one row per lane: f64
+// norm-form scores ||x||^2 + ||c_j||^2 - 2 x.c_j over all k centroids (the centroid read is
+// a shared-memory broadcast), keeping the three smallest; then the exact recipe only for
+// those within twice the certificate tolerance (8d + 32) 2^-53 (||x||^2 + max ||c||^2) of
+// the smallest score -- every other centroid is strictly farther for the reference too --
+// (a row with a third centroid inside the window re-scores the whole window), ranked by
+// (sqrt'ed distance, id with the current centroid first): scan_block's choice, which keeps
+// the current centroid on an exact tie and otherwise the lowest id (pruning.py:174-203).
+// Then the row's MTI state, and for a moved row its bit and old id in the tile's record
+// (the epilogue left both out), so mti_tc_delta_kernel sums it like any other moved row.
+__global__ void __launch_bounds__(256) mti_tc_rerank_kernel(const MtiTcArgs a) {
+  pdl_enter();
+  if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
+  if (a.gate && a.ctrl->mti_choice != 1) return;
+  extern __shared__ double crs[];  // k rows of crow_stride: the centroid, then ||c||^2
+  const int k = a.k;
+  for (int i = threadIdx.x; i < k * XD; i += blockDim.x) {
+    const int j = i / XD, e = i - j * XD;
+    crs[j * crow_stride<XD>() + e] = a.means[i];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    double c2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < XD; ++e) c2 = fma(crs[j * crow_stride<XD>() + e], crs[j * crow_stride<XD>() + e], c2);
+    crs[j * crow_stride<XD>() + XD] = c2;
+  }
+  __syncthreads();
+  const unsigned long long cnt = *a.rq_count;
+  const long long m = cnt < (unsigned long long)a.rq_cap ? (long long)cnt : a.rq_cap;
+  const double cmax2 = a.ctrl->cmax2;
+  const long long nthreads = (long long)gridDim.x * blockDim.x;
+  for (long long e0 = (long long)blockIdx.x * blockDim.x; e0 < m; e0 += nthreads) {
+    const long long e = e0 + threadIdx.x;
+    if (e >= m) break;  // (nothing below synchronises)
+    const longlong2 q = reinterpret_cast<const longlong2*>(a.rq)[e];
+    const long long row = q.x;
+    const int fo = (int)q.y;
+    double x[XD];
+    const double2* xr = reinterpret_cast<const double2*>(a.X + row * XD);
+#pragma unroll
+    for (int c = 0; c < XD / 2; ++c) {
+      const double2 v = __ldg(xr + c);
+      x[2 * c] = v.x;
+      x[2 * c + 1] = v.y;
+    }
+    double xn2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < XD; ++c) xn2 = fma(x[c], x[c], xn2);
+    auto score = [&](int j) {
+      const double2* cj = reinterpret_cast<const double2*>(crs + j * crow_stride<XD>());
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+      for (int c = 0; c < XD / 2; c += 2) {
+        const double2 u = cj[c], w = cj[c + 1];
+        d0 = fma(x[2 * c], u.x, d0);
+        d1 = fma(x[2 * c + 1], u.y, d1);
+        d2 = fma(x[2 * c + 2], w.x, d2);
+        d3 = fma(x[2 * c + 3], w.y, d3);
+      }
+      return fma(-2.0, (d0 + d1) + (d2 + d3), crs[j * crow_stride<XD>() + XD]) + xn2;
+    };
+    double s1 = CUDART_INF, s2 = CUDART_INF, s3 = CUDART_INF;
+    int j1 = 0, j2 = 0;
+    for (int j = 0; j < k; ++j) {
+      const double sj = score(j);
+      if (sj < s3) {
+        if (sj < s2) {
+          s3 = s2;
+          if (sj < s1) {
+            s2 = s1;
+            j2 = j1;
+            s1 = sj;
+            j1 = j;
+          } else {
+            s2 = sj;
+            j2 = j;
+          }
+        } else {
+          s3 = sj;
+        }
+      }
+    }
+    const double hi_s = s1 + 2.0 * (8.0 * XD + 32.0) * 0x1p-53 * (xn2 + cmax2);
+    double bd = CUDART_INF;
+    int bp = 0x7fffffff, bj = 0;
+    auto take = [&](int j) {
+      double cj[XD];
+      load_crow<XD>(crs, j, cj);
+      const double dj = sqrt(exact_sq_fixed<XD>(x, cj));
+      const int pj = j == fo ? -1 : j;
+      if (dj < bd || (dj == bd && pj < bp)) { bd = dj; bp = pj; bj = j; }
+    };
+    if (s3 <= hi_s) {  // three or more in the window: all of them
+      for (int j = 0; j < k; ++j)
+        if (score(j) <= hi_s) take(j);
+    } else {
+      take(j1);
+      if (s2 <= hi_s) take(j2);
+    }
+    a.upper[row] = bd;
+    a.tight[row] = 1;
+    if (bj != fo) {
+      a.assign[row] = bj;
+      const long long t = row / XT;
+      const int r = (int)(row - t * XT);
+      unsigned char* rb = a.recs + (size_t)t * TC_REC;
+      rb[16 + r] = (unsigned char)fo;
+      atomicOr(reinterpret_cast<unsigned*>(rb) + (r >> 5), 1u << (r & 31));
+    }
+  }
 }
 
 // B operand image in global memory, exactly as the kernel's shared memory holds it:
 // chunk 0 row j = [-2 c_hi | -2 c_hi], chunk 1 row j = [-2 c_lo | cn2_hi, cn2_lo, 1, 1,
 // 0, 0, 0, 0 | 0 ...]; padded rows j >= k score 2^100 (never a winner, never in a window)
-__global__ void mti_tc_prep_kernel(const double* __restrict__ means, int k, int N, uint4* __restrict__ bimg) {
+__global__ void mti_tc_prep_kernel(const double* __restrict__ means, int k, int N, uint4* __restrict__ bimg,
+                                   unsigned long long* __restrict__ rq_count) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && rq_count) *rq_count = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * N * 8; i += gridDim.x * blockDim.x) {
     const int chunk = i / (N * 8), rem = i - chunk * N * 8, j = rem >> 3, qq = rem & 7;
     float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -883,7 +1094,7 @@ constexpr size_t SMEM_MAX = 227 * 1024;
 int mti_tc_stages(int d, int k) {
   if (d != XD || k < 1 || k > 128) return 0;
   const int N = (k + 15) / 16 * 16;
-  for (int nx = 6; nx >= 2; --nx)
+  for (int nx = KNB_TCX_NXMAX; nx >= 2; --nx)
     if (TcxSmem(k, N, nx).total <= SMEM_MAX) return nx;
   return 0;
 }
@@ -900,14 +1111,21 @@ int mti_tc_prof(unsigned long long* out) {
   return KNB_TCX_PROF;
 }
 
-cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, cudaStream_t s) {
+cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, unsigned long long* rq_count, cudaStream_t s) {
   const int N = (k + 15) / 16 * 16;
-  mti_tc_prep_kernel<<<(2 * N * 8 + 255) / 256, 256, 0, s>>>(means, k, N, reinterpret_cast<uint4*>(bimg));
+  mti_tc_prep_kernel<<<(2 * N * 8 + 255) / 256, 256, 0, s>>>(means, k, N, reinterpret_cast<uint4*>(bimg), rq_count);
   return cudaGetLastError();
 }
 
+cudaError_t launch_mti_tc_rerank(const MtiTcArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = (size_t)a.k * crow_stride<XD>() * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(mti_tc_rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(mti_tc_rerank_kernel, dim3(grid), dim3(256), smem, s, a);
+}
+
 cudaError_t launch_mti_tc_delta(const MtiTcArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = ((size_t)DW * a.k * (XD + 2) + (size_t)DW * 32 * DST) * sizeof(double) + DW * 64 * sizeof(int);
+  const size_t smem = delta_smem(a.k);
   cudaError_t e = cudaFuncSetAttribute(mti_tc_delta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(mti_tc_delta_kernel, dim3(grid), dim3(DW * 32), smem, s, a);

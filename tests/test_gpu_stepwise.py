@@ -36,9 +36,25 @@ def _rows(name):
     return torch.from_numpy(c["data"](c["n"])).cuda()
 
 
+def _c4_rows(off, rows):
+    # the c4 stream at row `off`: PCG64 jump-ahead (16 doubles per row), as the fixture's maker did
+    bg = np.random.PCG64(np.random.SeedSequence(4))
+    bg.advance(off * 16)
+    return np.random.Generator(bg).random((rows, 16))
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_full_size_stepwise_parity(name):
+    """Replays the full-size run.  At the checked passes each shard's assignments are compared
+    with the pinned oracle's (oracle/lloyd.py lloyd_step: the reference recipe, pinned bit-exact
+    to numakmeans by tests/test_oracle_pins.py) against the centroids C_t this run used, and --
+    while the run reproduces the recorded one bit for bit (C_t sha256) -- with the REFERENCE's
+    own assignments stored in the fixture, plus the recorded per-pass counters.  A kernel change
+    that reorders the deterministic sums (new C_t bits) keeps the oracle check and drops the
+    recorded-run comparisons until oracle/make_golden_stepwise.py refreshes the fixture."""
     import torch
+
+    from oracle.lloyd import lloyd_step  # checker only
 
     g = _golden(name)
     c = kb.synth.CONFIGS[name]
@@ -48,31 +64,50 @@ def test_full_size_stepwise_parity(name):
     steps = [int(s) for s in g["steps"]]
     offs = [int(o) for o in g["shard_offsets"]]
     rows = int(g["shard_rows"])
+    eps = float(g["eps"])
+    shards = []
+    for o in offs:
+        dev = x[o:o + rows].cpu().numpy()
+        if name == "c4":
+            assert np.array_equal(dev, _c4_rows(o, rows)), "device rows differ from the PCG64 stream"
+        shards.append(dev.astype(np.float64))
+    recorded = True  # this run has reproduced the recorded one so far
     try:
         t = 0
         while True:
             cent = run.ctx.centroids()[0]
-            assert hashlib.sha256(np.ascontiguousarray(cent).tobytes()).hexdigest() == str(g["centroid_sha"][t]), \
-                f"{name}: centroids of pass {t} differ from the recorded run"
+            recorded = recorded and hashlib.sha256(np.ascontiguousarray(cent).tobytes()).hexdigest() == \
+                str(g["centroid_sha"][t])
             run.step()
             if t in steps:
                 si = steps.index(t)
                 a = run.ctx.assignments()
                 for j, o in enumerate(offs):
                     got = a[o:o + rows]
-                    want = g["ref_assign"][si, j]
-                    bad = np.flatnonzero(got != want)
-                    assert np.all(g["near_tie"][si, j][bad]), \
-                        f"{name} pass {t} shard {o}: {int((~g['near_tie'][si, j][bad]).sum())} non-near-tie mismatches"
+                    ids, d1, d2 = lloyd_step(shards[j], cent)
+                    tie = (d2 - d1) / np.maximum(d2, 1e-300) < eps
+                    bad = np.flatnonzero(got != ids)
+                    assert np.all(tie[bad]), \
+                        f"{name} pass {t} shard {o}: {int((~tie[bad]).sum())} non-near-tie mismatches vs the oracle"
+                    if recorded:
+                        want = g["ref_assign"][si, j]
+                        bad = np.flatnonzero(got != want)
+                        assert np.all(g["near_tie"][si, j][bad]), \
+                            f"{name} pass {t} shard {o}: {int((~g['near_tie'][si, j][bad]).sum())} " \
+                            "non-near-tie mismatches vs the reference"
             t += 1
             if run.ctx.state()["stop"]:
                 break
         stats = run.ctx.stats()
         assert len(stats) == c["max_iters"] == len(g["reassignments"])
-        np.testing.assert_array_equal([s.reassignments for s in stats], g["reassignments"])
-        np.testing.assert_array_equal([s.skips for s in stats], g["skips"])
-        np.testing.assert_array_equal(run.ctx.centroids()[2], g["counts"])
         assert int(run.ctx.centroids()[2].sum()) == c["n"]
+        if recorded:
+            np.testing.assert_array_equal([s.reassignments for s in stats], g["reassignments"])
+            np.testing.assert_array_equal([s.skips for s in stats], g["skips"])
+            np.testing.assert_array_equal(run.ctx.centroids()[2], g["counts"])
+        else:
+            print(f"{name}: C_t differ from the recorded run (summation order changed): "
+                  "checked against the oracle only")
     finally:
         run.close()
         del x
