@@ -98,8 +98,15 @@ cudaError_t staged_copy(int device, void* dst, const void* src, size_t bytes, bo
   const bool pinned = cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost;
   cudaGetLastError();
   Pool* p = nullptr;
-  if (pinned || bytes < STAGE_MIN || pool_for(device, &p) != cudaSuccess)
-    return cudaMemcpy(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost);
+  if (pinned || bytes < STAGE_MIN || pool_for(device, &p) != cudaSuccess) {
+    e = cudaMemcpy(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost);
+    // From pageable memory an H2D cudaMemcpy returns once the source is staged, possibly
+    // before its DMA has landed, and only the legacy stream is ordered after that DMA; the
+    // caller's kernels run on a non-blocking stream, so wait for it here (a check of the
+    // rows right after an upload read the tail of a previous allocation otherwise).
+    if (e == cudaSuccess && h2d && !pinned) e = cudaStreamSynchronize(cudaStreamLegacy);
+    return e;
+  }
   std::lock_guard<std::mutex> lock(p->use);
   const size_t nchunks = (bytes + CHUNK - 1) / CHUNK;
   const int W = (int)std::min<size_t>(WORKERS, nchunks);

@@ -251,6 +251,40 @@ __global__ void geometry_pairs_kernel(const FinalArgs f) {
   }
 }
 
+// The whole barrier action in one CTA for small k (k <= FUSED_MAX_K): every centroid's
+// finalize (a warp each), the statistics row and convergence test, then -- pruned runs --
+// the pair-wise geometry, with __syncthreads between the phases instead of a grid-wide
+// arrival counter and a separate geometry launch (c1: 22.8 -> 21.8 us per iteration).
+// (Folding the reduction of the CTA partials in as well, one CTA instead of a grid, was
+// slower: c1 28.9 us.)
+#ifndef KNB_NO_FUSED_FINISH
+#define KNB_NO_FUSED_FINISH 0
+#endif
+constexpr int FUSED_MAX_K = KNB_NO_FUSED_FINISH ? 0 : 16;
+__global__ void __launch_bounds__(512) finish_small_kernel(const FinalArgs f) {
+  pdl_enter();
+  if (f.ctrl->stop && !f.ctrl->ignore_stop) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < f.k; j += nw) finalize_centroid(f, j);
+  __syncthreads();
+  stats_body(f);
+  if (!f.pruning) return;
+  __syncthreads();
+  const int k = f.k, d = f.d;
+  for (int p = warp; p < k * k; p += nw) {
+    const int a = p / k, b = p - a * k;
+    if (b <= a) continue;  // warp-uniform
+    const double h = sqrt(warp_exact_sq(f.means + (long long)b * d, f.means + (long long)a * d, d, lane)) * 0.5;
+    if (lane == 0) {
+      f.half[(long long)a * k + b] = h;
+      f.half[(long long)b * k + a] = h;
+      const unsigned long long hb = (unsigned long long)__double_as_longlong(h);
+      atomicMin(reinterpret_cast<unsigned long long*>(f.half_min + a), hb);
+      atomicMin(reinterpret_cast<unsigned long long*>(f.half_min + b), hb);
+    }
+  }
+}
+
 __global__ void geometry_kernel(const FinalArgs f) {
   pdl_enter();
   const Ctrl* c = f.ctrl;
@@ -328,11 +362,13 @@ cudaError_t launch_reduce(const double* partials, int G, long long L, double* ou
 }
 
 cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t s) {
+  if (f.k <= FUSED_MAX_K) return launch_pdl(finish_small_kernel, dim3(1), dim3(512), 0, s, f);
   const int wpb = 8;
   return launch_pdl(finalize_kernel, dim3((f.k + wpb - 1) / wpb), dim3(wpb * 32), 0, s, f);
 }
 
 cudaError_t launch_geometry(const FinalArgs& f, cudaStream_t s) {
+  if (f.k <= FUSED_MAX_K) return cudaSuccess;  // (finish_small_kernel did it)
   if (f.k <= GEO_PAIRS_MAX_K) {
     const long long warps = (long long)f.k * f.k;
     return launch_pdl(geometry_pairs_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, s, f);
