@@ -61,6 +61,10 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
                int32_t k, int32_t pruning, int32_t max_iters, double tolerance, void* stream,
                knb_ctx** out);
 int knb_destroy(knb_ctx* ctx);
+/* Device memory of destroyed contexts stays in the library's pool for the next context
+ * (no reference counterpart: the reference allocates numpy arrays per call).  This hands
+ * the unused part back to the driver -- torch.cuda.empty_cache's counterpart. */
+int knb_release_memory(int device);
 
 /* Rows of the shard: copy from host (any pointer; pinned is faster) into a context-owned
  * buffer, or attach caller-owned device rows.  Replaces _MemorySource (engine.py:162-191). */

@@ -24,6 +24,7 @@ from .engine import (
 from .fileio import HEADER_SIZE, MatrixIOError, load_matrix, save_matrix
 from .matrix import MatrixFormatError, RowRange, check_matrix, partition_rows
 from .outofcore import CacheSchedule, RowStore, kmeans_ondisk
+from ._native import release_memory
 from .parallel import LocalComm, TorchComm, shard_of
 from .primitives import (
     CentroidGeometry,
@@ -73,6 +74,7 @@ __all__ = [
     "check_matrix",
     "kmeans",
     "kmeans_sharded",
+    "release_memory",
     "partition_rows",
     "shard_of",
 ]

@@ -53,6 +53,7 @@ SIGNATURES = {
     "knb_device_info": [ctypes.c_int, _PI32, _PI64, _PI32, _PI32],
     "knb_create": [ctypes.c_int, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _D, _P, ctypes.POINTER(_P)],
     "knb_destroy": [_P],
+    "knb_release_memory": [ctypes.c_int],
     "knb_upload_rows": [_P, _P, _I64, _I64],
     "knb_attach_rows": [_P, _P],
     "knb_attach_host_rows": [_P, _P],
@@ -420,6 +421,12 @@ def mti_compact_ok(n_local: int) -> bool:
     """Whether a shard of n_local rows may run the compacted MTI kernel (32-bit row
     indices); larger shards run the block-dense MTI pass (same results)."""
     return bool(lib().knb_mti_compact_ok(int(n_local)))
+
+
+def release_memory(device: int = 0) -> None:
+    """Return the device memory the library's pool holds but no context uses to the driver
+    (the pool keeps it between kmeans() calls, as torch's caching allocator does)."""
+    check(lib().knb_release_memory(int(device)))
 
 
 def reserve_staging(device: int = 0) -> None:

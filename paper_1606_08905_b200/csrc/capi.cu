@@ -8,10 +8,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <mutex>
 #include <unordered_map>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -149,8 +151,11 @@ namespace {
 // One stream-ordered memory pool per device for every context's buffers: a context's
 // create / destroy then costs no cudaMalloc / cudaFree (each an implicit device
 // synchronisation) once the pool holds the memory -- repeated kmeans() calls reuse it.
-// Up to 16 GiB stays reserved between contexts; beyond that the pool returns memory to
-// the driver at the next synchronisation.
+// Like torch's caching allocator, the pool keeps what it has mapped (returning ~100 GB to
+// the driver took 0.6-0.8 s inside knb_destroy, i.e. inside every large kmeans() call;
+// a background trim instead contended with the next call's mapping): knb_release_memory
+// hands the unused part back (Python: release_memory(), as torch.cuda.empty_cache), and
+// the pool's unused memory is reused by the next context's allocations.
 cudaMemPool_t lib_pool(int device) {
   static std::mutex mu;
   static std::unordered_map<int, cudaMemPool_t> pools;
@@ -166,7 +171,7 @@ cudaMemPool_t lib_pool(int device) {
     cudaGetLastError();
     pool = nullptr;
   } else {
-    uint64_t keep = 16ULL << 30;
+    uint64_t keep = ~0ULL;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   pools[device] = pool;
@@ -884,6 +889,15 @@ int knb_destroy(knb_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  return KNB_OK;
+}
+
+int knb_release_memory(int device) {
+  KNB_CUDA(cudaSetDevice(device));
+  if (cudaMemPool_t pool = lib_pool(device)) {
+    KNB_CUDA(cudaDeviceSynchronize());
+    KNB_CUDA(cudaMemPoolTrimTo(pool, 0));
+  }
   return KNB_OK;
 }
 

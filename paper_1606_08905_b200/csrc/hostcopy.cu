@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <cstdlib>
 #include <unordered_map>
 #include <vector>
 
@@ -26,8 +27,23 @@ namespace knb {
 
 namespace {
 
-constexpr size_t CHUNK = 8ull << 20;  // bytes per pinned chunk
-constexpr int WORKERS = 8;
+// chunk size and worker count: KNB_STAGE_CHUNK_MB / KNB_STAGE_WORKERS override the
+// defaults (read once, when the pool is built)
+size_t g_chunk = 8ull << 20;  // bytes per pinned chunk
+int g_workers = 8;
+void read_stage_env() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (const char* v = std::getenv("KNB_STAGE_CHUNK_MB")) {
+    const long mb = std::atol(v);
+    if (mb >= 1 && mb <= 256) g_chunk = (size_t)mb << 20;
+  }
+  if (const char* v = std::getenv("KNB_STAGE_WORKERS")) {
+    const int w = std::atoi(v);
+    if (w >= 1 && w <= 64) g_workers = w;
+  }
+}
 
 struct Pool {
   std::vector<char*> buf;           // 2 per worker
@@ -46,16 +62,17 @@ cudaError_t pool_for(int device, Pool** out) {
     *out = it->second;
     return cudaSuccess;
   }
+  read_stage_env();
   Pool* p = new Pool();
   cudaError_t e = cudaSuccess;
-  for (int w = 0; w < WORKERS && e == cudaSuccess; ++w) {
+  for (int w = 0; w < g_workers && e == cudaSuccess; ++w) {
     cudaStream_t s = nullptr;
     e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     if (e != cudaSuccess) break;
     p->stream.push_back(s);
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
       char* h = nullptr;
-      e = cudaHostAlloc(reinterpret_cast<void**>(&h), CHUNK, cudaHostAllocPortable);
+      e = cudaHostAlloc(reinterpret_cast<void**>(&h), g_chunk, cudaHostAllocPortable);
       if (e != cudaSuccess) break;
       p->buf.push_back(h);
       cudaEvent_t ev = nullptr;
@@ -108,8 +125,9 @@ cudaError_t staged_copy(int device, void* dst, const void* src, size_t bytes, bo
     return e;
   }
   std::lock_guard<std::mutex> lock(p->use);
+  const size_t CHUNK = g_chunk;
   const size_t nchunks = (bytes + CHUNK - 1) / CHUNK;
-  const int W = (int)std::min<size_t>(WORKERS, nchunks);
+  const int W = (int)std::min<size_t>((size_t)p->stream.size(), nchunks);
   std::atomic<int> err{(int)cudaSuccess};
   auto worker = [&](int w) {
     cudaError_t le = cudaSetDevice(device);

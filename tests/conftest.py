@@ -32,6 +32,18 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+@pytest.fixture(autouse=True)
+def _release_device_memory(request):
+    """After each GPU test, hand the library pool's unused device memory back (it keeps it
+    between kmeans() calls, like torch's caching allocator), so the next test's torch
+    allocations see it free."""
+    yield
+    if request.node.get_closest_marker("gpu") is not None:
+        from paper_1606_08905_b200 import _native
+        if _native._lib is not None:
+            _native.release_memory(0)
+
+
 def has_gpu() -> bool:
     try:
         import torch
