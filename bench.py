@@ -345,7 +345,9 @@ def run_ours(args):
     fp_peak = tf32_peak if tc else 2 * dfma_peak
     t_fp = flops / fp_peak
     t_hbm = bytes_ / (hbm_peak * 1e9)
-    tcx = (not tc) and cfg["pruning"] and run.ctx.mti_tc_info()["available"]  # f64 rows, tcgen05 MTI pass
+    # f64 rows on the tcgen05 MTI pass: rows of 16 (automatic choice), or any supported row
+    # width when forced with --mti-scan tc
+    tcx = (not tc) and cfg["pruning"] and run.ctx.mti_tc_info()["available"] and (d == 16 or args.mti_scan == "tc")
     if tc:
         roof = {"bound": "tensor", "achieved": flops / kern_s / 1e12, "peak": fp_peak / 1e12,
                 "unit": "TFLOP/s", "peak_source": "0.5 x MEASURED_PEAKS.json bf16_tflops (kind::tf32 = half the "

@@ -234,10 +234,17 @@ FinalArgs final_args(knb_ctx* c) {
 }
 
 // fresh run state: iteration 0, not stopped, assignment zero, running sums zero
+bool tcx_ready(const knb_ctx* c);
+
 int reset_run(knb_ctx* c) {
   Ctrl h;
   std::memset(&h, 0, sizeof(h));
   h.full_pass = 1;
+  // the pruned pass streams every row (tcgen05 pass, or the DMMA block pass) while clause 1
+  // skips fewer than this share of rows, and compacts the survivors above it (measured: the
+  // tcgen05 pass at c2's 49% / c3's 41% skips runs 0.226 / 2.16 ms against the compacted
+  // DMMA pass's 0.167 / 1.22 ms -- its per-row epilogue work does not shrink with skips)
+  h.block_pct = 10;
   h.max_iters = c->max_iters;
   h.tolerance = c->tolerance;
   KNB_CUDA(cudaMemcpyAsync(c->ctrl, &h, offsetof(Ctrl, cmax2), cudaMemcpyHostToDevice, c->stream));
@@ -284,11 +291,13 @@ int build_tmap(knb_ctx* c) {
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r == CUDA_SUCCESS) c->use_tma = 1;
   c->tcx_map = false;
-  if (c->use_tma && c->tcx_nx > 0) {  // the tcgen05 MTI pass: 128-row boxes, same swizzle
-    cuuint32_t box128[2] = {16u, 128u};
+  if (c->use_tma && c->tcx_nx > 0) {
+    // the tcgen05 MTI pass: 128-row boxes, 16 columns (128 B, SWIZZLE_128B; d = 32 takes
+    // two per tile) or the whole 8-column row (64 B, SWIZZLE_64B)
+    cuuint32_t box128[2] = {c->d == 8 ? 8u : 16u, 128u};
     r = encode(&c->tmX128, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(c->X), gdim, gstride, box128,
-               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, c->d == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     c->tcx_map = r == CUDA_SUCCESS;
   }
   return KNB_OK;
@@ -512,7 +521,7 @@ bool tcx_ready(const knb_ctx* c) {
 }
 
 int launch_tcx(knb_ctx* c, int gate, float* dbg) {
-  KNB_CUDA(launch_mti_tc_prep(c->means, c->k, c->tcx_bimg, dbg ? nullptr : c->tcx_rq_count, c->stream));
+  KNB_CUDA(launch_mti_tc_prep(c->means, c->d, c->k, c->tcx_bimg, dbg ? nullptr : c->tcx_rq_count, c->stream));
   MtiTcArgs t;
   t.X = c->X;
   t.n = c->n_local;
@@ -609,9 +618,12 @@ int launch_pass(knb_ctx* c) {
   m.cache = c->semA.cache;
   m.gate = 0;
   int mode = (c->mti_mma_ok || c->mti_scan == KNB_MTI_TC) ? c->mti_scan : KNB_MTI_EXACT;
-  const bool tcx = tcx_ready(c);
-  if (mode == KNB_MTI_TC && !tcx)
-    return fail(KNB_E_ARG, "the tcgen05 MTI pass needs d == 16, k <= 128 and 16-byte aligned rows in HBM");
+  const bool tcx_any = tcx_ready(c);
+  // automatic choices take the tcgen05 pass for rows of 16 (config 4: 148.6 -> 45 ms per
+  // pass against the DMMA block pass); rows of 8 / 32 run it when forced (mti_scan="tc")
+  const bool tcx = tcx_any && (c->d == 16 || mode == KNB_MTI_TC);
+  if (mode == KNB_MTI_TC && !tcx_any)
+    return fail(KNB_E_ARG, "the tcgen05 MTI pass needs d in {8, 16, 32}, k <= 128 (k <= 32 for d = 32) and 16-byte aligned rows in HBM");
   // the compacted kernel's filter uses 32-bit row / block indices: larger shards take a
   // block MTI pass (64-bit indices, same results)
   if ((mode == KNB_MTI_AUTO || mode == KNB_MTI_DENSE) && !mti_compact_ok(c->n_local))
@@ -833,7 +845,7 @@ int knb_create(int device, int64_t n_global, int64_t n_local, int64_t row_lo, in
   if (c->tcx_nx > 0) {
     if ((rc = dev_alloc(c, &c->tcx_counters, 1))) return bail(rc);
     double* bimg = nullptr;
-    if ((rc = dev_alloc(c, &bimg, mti_tc_bimg_bytes(k) / sizeof(double)))) return bail(rc);
+    if ((rc = dev_alloc(c, &bimg, mti_tc_bimg_bytes(d, k) / sizeof(double)))) return bail(rc);
     c->tcx_bimg = bimg;
     double* recs = nullptr;
     const size_t rec_bytes = (size_t)((nl + 127) / 128) * TC_REC;
@@ -1571,7 +1583,7 @@ int knb_set_option(knb_ctx* c, int32_t option, int64_t value) {
   if (option == KNB_OPT_MTI_SCAN) {
     if (value < KNB_MTI_AUTO || value > KNB_MTI_TC) return fail(KNB_E_ARG, "bad MTI scan mode");
     if (value == KNB_MTI_TC && c->tcx_nx == 0)
-      return fail(KNB_E_ARG, "the tcgen05 MTI pass needs a pruned run with d == 16 and k <= 128");
+      return fail(KNB_E_ARG, "the tcgen05 MTI pass needs a pruned run with d in {8, 16, 32} and k <= 128 (k <= 32 for d = 32)");
     if ((value == KNB_MTI_DENSE || value == KNB_MTI_BLOCK) && !c->mti_mma_ok)
       return fail(KNB_E_ARG, "dense MTI scan needs d <= 64 and centroids that fit shared memory");
     c->mti_scan = (int)value;

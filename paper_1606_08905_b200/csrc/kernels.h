@@ -192,8 +192,9 @@ constexpr int TC_REC = 16 + 128;
 cudaError_t launch_mti_tc_delta(const MtiTcArgs& a, int grid, cudaStream_t s);
 int mti_tc_stages(int d, int k);
 int mti_tc_prof(unsigned long long* out);  // 16 counters; returns 1 in a -DKNB_TCX_PROF=1 build
-size_t mti_tc_bimg_bytes(int k);
-cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, unsigned long long* rq_count, cudaStream_t s);
+size_t mti_tc_bimg_bytes(int d, int k);
+cudaError_t launch_mti_tc_prep(const double* means, int d, int k, void* bimg, unsigned long long* rq_count,
+                               cudaStream_t s);
 cudaError_t launch_mti_tc_rerank(const MtiTcArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s);
 

@@ -71,16 +71,49 @@ namespace knb {
 namespace {
 
 constexpr int XT = 128;                        // rows per tile (UMMA M)
-constexpr int XD = 16;                         // dims
-constexpr uint32_t X_TILE = XT * XD * 8;       // f64 tile, 16 KB
-constexpr uint32_t A_CHUNK = XT * 128;         // the (x_hi | x_lo) K chunk of the operand tile, SW128
-#ifndef KNB_TCX_PLAIN
-#define KNB_TCX_PLAIN 0
-#endif
-// the norm constants [1, 1, xn2_hi, xn2_lo, 0 x 4]: a no-swizzle 32-byte-row tile, or a
-// 128-byte SW128 chunk
-constexpr uint32_t A_CONST = KNB_TCX_PLAIN ? XT * 32 : XT * 128;
-constexpr uint32_t A_TILE = A_CHUNK + A_CONST;
+constexpr uint32_t CH = XT * 128;              // one 128-byte-row SW128 operand chunk (16 KB)
+
+// Layouts per row width XD in {8, 16, 32} (configs 3, 4, 2).  The f64 stage is the
+// tile's rows as TMA wrote them: XD = 8 one 64-byte-wide box (SWIZZLE_64B), XD = 16 one
+// 128-byte box (SWIZZLE_128B), XD = 32 two 128-byte boxes (columns 0-15, 16-31).  The
+// TF32 operands are 128-byte K chunks (SWIZZLE_128B), one UMMA k-step = 8 tf32 = 32 B:
+//   XD = 8:  A = [x_hi | x_lo | x_hi | 1 1 xn2_hi xn2_lo 0 0 0 0]
+//            B = [-2c_hi | -2c_hi | -2c_lo | cn2_hi cn2_lo 1 1 0 0 0 0]      4 k-steps
+//   XD = 16: A = [x_hi | x_lo], [1 1 xn2_hi xn2_lo 0..]
+//            B = [-2c_hi | -2c_hi], [-2c_lo | cn2_hi cn2_lo 1 1 0..]          7 k-steps
+//   XD = 32: A = [x_hi], [x_lo], [1 1 xn2_hi xn2_lo 0..]
+//            B = [-2c_hi], [-2c_lo], [cn2_hi cn2_lo 1 1 0..]                  13 k-steps
+template <int XD>
+struct Geo {
+  static_assert(XD == 8 || XD == 16 || XD == 32, "row widths 8, 16, 32");
+  static constexpr uint32_t X_TILE = XT * XD * 8;         // f64 stage bytes
+  static constexpr int NTMA = XD == 32 ? 2 : 1;           // TMA boxes per tile
+  static constexpr int BOXW = XD == 8 ? 8 : 16;           // box width (doubles)
+  static constexpr int A_NCH = XD == 32 ? 3 : (XD == 16 ? 2 : 1);  // operand chunks (incl. constants)
+  static constexpr uint32_t A_TILE = A_NCH * CH;
+  static constexpr int B_NCH = A_NCH;
+  // the certificate's product / accumulation coefficients (2^-20 units): 6.4 for the split
+  // products, half a unit per f32 accumulation step
+  static constexpr float C1 = XD == 32 ? 20.0f : 12.5f;
+  static constexpr float C2 = XD == 32 ? 6.0f : 4.0f;
+};
+
+// byte offset of 16-byte chunk q (0 .. XD/2 - 1) of row r in the f64 stage
+template <int XD>
+__device__ __forceinline__ uint32_t xoff(int r, int q) {
+  if constexpr (XD == 8) return (uint32_t)r * 64u + ((uint32_t)((q ^ (r >> 1)) & 3) << 4);
+  else if constexpr (XD == 16) return (uint32_t)r * 128u + ((uint32_t)((q ^ r) & 7) << 4);
+  else return (uint32_t)(q >> 3) * CH + (uint32_t)r * 128u + ((uint32_t)(((q & 7) ^ r) & 7) << 4);
+}
+// row r of a stage read element by element (exact_sq_fixed's x operand, no register copy)
+template <int XD>
+struct StageRow {
+  const unsigned char* xs;
+  int r;
+  __device__ __forceinline__ double operator[](int i) const {
+    return *reinterpret_cast<const double*>(xs + xoff<XD>(r, i >> 1) + (i & 1) * 8);
+  }
+};
 #ifndef KNB_TCX_PF
 #define KNB_TCX_PF 6
 #endif
@@ -130,15 +163,16 @@ constexpr int NACC = KNB_TCX_NACC;
 
 __host__ __device__ inline uint32_t al(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
+template <int XD>
 struct TcxSmem {
   uint32_t x0, a0, b0, crow, hd, ebuf, bars, total;
   int NX;
   __host__ __device__ TcxSmem(int k, int N, int nx) {
     NX = nx;
     uint32_t o = 0;
-    a0 = o;   o += NA * A_TILE;
-    x0 = o;   o += nx * X_TILE;
-    b0 = o;   o += 2u * N * 128u;
+    a0 = o;   o += NA * Geo<XD>::A_TILE;
+    x0 = o;   o += nx * Geo<XD>::X_TILE;
+    b0 = o;   o += (uint32_t)Geo<XD>::B_NCH * N * 128u;
     crow = o; o += (uint32_t)k * crow_stride<XD>() * 8u;
     hd = o;   o += (uint32_t)k * 16u;
     ebuf = o; o += (uint32_t)NE * XT * 4u;
@@ -286,17 +320,18 @@ __device__ __forceinline__ void min2_keys(const int (&key)[W], int& gm, int& g2)
   g2 = (int)((uint32_t)gm + 1u + min(min(c[0], c[1]), min(c[2], c[3])));
 }
 
-template <int NG, int LAST>
+template <int XD, int NG, int LAST>
 __global__ void __maxnreg__(KNB_TCX_REGS)
     mti_tc_kernel(const __grid_constant__ CUtensorMap tmX, const MtiTcArgs a) {
   constexpr int N = 16 * NG;
+  using G = Geo<XD>;
   pdl_enter();
   if (!a.dbg && a.ctrl->stop && !a.ctrl->ignore_stop) return;  // (the score dump ignores the stop flag)
   if (a.gate && a.ctrl->mti_choice != 1) return;  // the compacted MTI kernel runs this iteration
   extern __shared__ unsigned char smem_raw[];
   unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int k = a.k;
-  const TcxSmem L(k, N, a.nx);
+  const TcxSmem<XD> L(k, N, a.nx);
   const int NX = L.NX;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
@@ -316,7 +351,7 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.bimg);
     uint4* dst = reinterpret_cast<uint4*>(sm + L.b0);
-    for (int i = tid; i < 2 * N * 8; i += THREADS) dst[i] = src[i];
+    for (int i = tid; i < G::B_NCH * N * 8; i += THREADS) dst[i] = src[i];
     for (int i = tid; i < k * XD; i += THREADS) {
       const int j = i / XD, e = i - j * XD;
       crow[j * crow_stride<XD>() + e] = a.means[i];
@@ -362,14 +397,17 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       ProfClock pc;
       pc.start();
       // the f64 tiles, each pulled into L2 PF tiles before its TMA load
-      for (int i = 0; i < PF && i < mine; ++i) tma_prefetch_l2_2d(&tmX, 0, (t0 + i * tstep) * XT);
+      for (int i = 0; i < PF && i < mine; ++i)
+        for (int t = 0; t < G::NTMA; ++t) tma_prefetch_l2_2d(&tmX, t * 16, (t0 + i * tstep) * XT);
       int s = 0, ph = 0;
       for (int i = 0; i < mine; ++i) {
-        if (i + PF < mine) tma_prefetch_l2_2d(&tmX, 0, (t0 + (i + PF) * tstep) * XT);
+        if (i + PF < mine)
+          for (int t = 0; t < G::NTMA; ++t) tma_prefetch_l2_2d(&tmX, t * 16, (t0 + (i + PF) * tstep) * XT);
         mbar_sleep(x_empty + s, ph ^ 1);
         pc.lap(0);
-        mbar_arrive_expect_tx(x_full + s, X_TILE);
-        tma_load_2d(sm + L.x0 + s * X_TILE, &tmX, x_full + s, 0, (t0 + i * tstep) * XT);
+        mbar_arrive_expect_tx(x_full + s, G::X_TILE);
+        for (int t = 0; t < G::NTMA; ++t)
+          tma_load_2d(sm + L.x0 + s * G::X_TILE + t * CH, &tmX, x_full + s, t * 16, (t0 + i * tstep) * XT);
         pc.lap(1);
         if (++s == NX) { s = 0; ph ^= 1; }
       }
@@ -390,18 +428,37 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
         pc.lap(1);
         tc_fence_after();
         const uint32_t dt = tmem + b * TCOLS;
-        const uint32_t A0 = smem_u32(sm + L.a0 + sa * A_TILE), AC = A0 + A_CHUNK;
-        // (x_hi | x_lo) . (c_hi | c_hi)
+        const uint32_t A0 = smem_u32(sm + L.a0 + sa * G::A_TILE);
+        if constexpr (XD == 8) {
+          // x_hi.c_hi, x_lo.c_hi, x_hi.c_lo, [1, 1, xn2_hi, xn2_lo].[cn2_hi, cn2_lo, 1, 1]
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b0 + ks * 32), idesc, ks > 0);
-        // x_hi . c_lo
+          for (int ks = 0; ks < 4; ++ks)
+            umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b0 + ks * 32), idesc, ks > 0);
+        } else if constexpr (XD == 16) {
+          const uint32_t AC = A0 + CH;
+          // (x_hi | x_lo) . (c_hi | c_hi)
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-          umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b1 + ks * 32), idesc, 1);
-        // [1, 1, xn2_hi, xn2_lo] . [cn2_hi, cn2_lo, 1, 1]
-        umma_tf32(dt, KNB_TCX_PLAIN ? umma_desc_plain(AC, 128, 256) : umma_desc_sw128(AC), umma_desc_sw128(b1 + 2 * 32),
-                  idesc, 1);
+          for (int ks = 0; ks < 4; ++ks)
+            umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b0 + ks * 32), idesc, ks > 0);
+          // x_hi . c_lo
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b1 + ks * 32), idesc, 1);
+          // [1, 1, xn2_hi, xn2_lo] . [cn2_hi, cn2_lo, 1, 1]
+          umma_tf32(dt, umma_desc_sw128(AC), umma_desc_sw128(b1 + 2 * 32), idesc, 1);
+        } else {
+          const uint32_t A1 = A0 + CH, AC = A0 + 2 * CH, b2 = b1 + N * 128;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)  // x_hi . c_hi
+            umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b0 + ks * 32), idesc, ks > 0);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)  // x_lo . c_hi
+            umma_tf32(dt, umma_desc_sw128(A1 + ks * 32), umma_desc_sw128(b0 + ks * 32), idesc, 1);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)  // x_hi . c_lo
+            umma_tf32(dt, umma_desc_sw128(A0 + ks * 32), umma_desc_sw128(b1 + ks * 32), idesc, 1);
+          umma_tf32(dt, umma_desc_sw128(AC), umma_desc_sw128(b2), idesc, 1);
+        }
         umma_commit(a_empty + sa);
         umma_commit(t_full + b);
         pc.lap(2);
@@ -423,39 +480,70 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       pc.lap(0);
       mbar_sleep(a_empty + sa, ((i / NA) & 1) ^ 1);
       pc.lap(1);
-      const unsigned char* xs = sm + L.x0 + s * X_TILE;
-      unsigned char* A0 = sm + L.a0 + sa * A_TILE;
-      unsigned char* AC = A0 + A_CHUNK;
+      const unsigned char* xs = sm + L.x0 + s * G::X_TILE;
+      unsigned char* A0 = sm + L.a0 + sa * G::A_TILE;
 #pragma unroll
       for (int rr = 0; rr < ((KNB_TCX_ABL & 1) ? 0 : 4 / NCONV); ++rr) {
       const int r = r0 + rr * 32 * NCONV;
-      float hi[XD], lo[XD];
       float n0 = 0.0f, n1 = 0.0f;
+      auto put = [&](unsigned char* base, int c, float v0, float v1, float v2, float v3) {
+        *reinterpret_cast<float4*>(base + swz(r, c)) = make_float4(v0, v1, v2, v3);
+      };
+      if constexpr (XD <= 16) {
+        // all loads and conversions first, then the operand stores (measured on c4: the
+        // interleaved form below runs the pass at 52 instead of 45 ms -- the converters are
+        // on the MMA's critical path); rows of 32 take the interleaved form (registers)
+        float hi[XD], lo[XD];
 #pragma unroll
-      for (int q = 0; q < XD / 2; ++q) {
-        const double2 v = *reinterpret_cast<const double2*>(xs + swz(r, q));
-        const float f0 = __double2float_rn(v.x), f1 = __double2float_rn(v.y);
-        hi[2 * q] = tf32_trunc(f0);
-        hi[2 * q + 1] = tf32_trunc(f1);
-        lo[2 * q] = f0 - hi[2 * q];
-        lo[2 * q + 1] = f1 - hi[2 * q + 1];
-        n0 = fmaf(f0, f0, n0);
-        n1 = fmaf(f1, f1, n1);
+        for (int q = 0; q < XD / 2; ++q) {
+          const double2 v = *reinterpret_cast<const double2*>(xs + xoff<XD>(r, q));
+          const float f0 = __double2float_rn(v.x), f1 = __double2float_rn(v.y);
+          hi[2 * q] = tf32_trunc(f0);
+          hi[2 * q + 1] = tf32_trunc(f1);
+          lo[2 * q] = f0 - hi[2 * q];
+          lo[2 * q + 1] = f1 - hi[2 * q + 1];
+          n0 = fmaf(f0, f0, n0);
+          n1 = fmaf(f1, f1, n1);
+        }
+#pragma unroll
+        for (int c = 0; c < XD / 4; ++c) {
+          put(A0, c, hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+          if constexpr (XD == 8) {
+            put(A0, c + 2, lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+            put(A0, c + 4, hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+          } else {
+            put(A0, c + 4, lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+          }
+        }
+      } else {
+        // four dims at a time: f32, the TF32 head (truncated), the f32 remainder, the norm
+#pragma unroll
+        for (int c = 0; c < XD / 4; ++c) {
+          const double2 v0 = *reinterpret_cast<const double2*>(xs + xoff<XD>(r, 2 * c));
+          const double2 v1 = *reinterpret_cast<const double2*>(xs + xoff<XD>(r, 2 * c + 1));
+          const float f0 = __double2float_rn(v0.x), f1 = __double2float_rn(v0.y);
+          const float f2 = __double2float_rn(v1.x), f3 = __double2float_rn(v1.y);
+          const float h0 = tf32_trunc(f0), h1 = tf32_trunc(f1), h2 = tf32_trunc(f2), h3 = tf32_trunc(f3);
+          n0 = fmaf(f0, f0, n0);
+          n1 = fmaf(f1, f1, n1);
+          n0 = fmaf(f2, f2, n0);
+          n1 = fmaf(f3, f3, n1);
+          put(A0, c, h0, h1, h2, h3);
+          put(A0 + CH, c, f0 - h0, f1 - h1, f2 - h2, f3 - h3);
+        }
       }
       const float xn2 = n0 + n1;  // (a row constant: its rounding shifts every D~_j alike)
       const float xh = tf32_trunc(xn2), xl = xn2 - xh;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        *reinterpret_cast<float4*>(A0 + swz(r, c)) = make_float4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
-        *reinterpret_cast<float4*>(A0 + swz(r, c + 4)) =
-            make_float4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+      {
+        unsigned char* AC = XD == 8 ? A0 : A0 + (Geo<XD>::A_NCH - 1) * CH;
+        const int q0 = XD == 8 ? 6 : 0;
+        put(AC, q0, 1.0f, 1.0f, xh, xl);
+        put(AC, q0 + 1, 0.0f, 0.0f, 0.0f, 0.0f);
       }
-      *reinterpret_cast<float4*>(AC + (KNB_TCX_PLAIN ? plain_off(r, 0) : swz(r, 0))) = make_float4(1.0f, 1.0f, xh, xl);
-      *reinterpret_cast<float4*>(AC + (KNB_TCX_PLAIN ? plain_off(r, 1) : swz(r, 1))) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       // the certificate's bound E(x) for the epilogue (f32 with a relative margin;
       // xn2 carries < 2^-20 relative error)
       const float xnb = xn2 * (1.0f + 0x1p-12f);
-      ebuf[(i & (NE - 1)) * XT + r] = (0x1p-20f * (12.5f * sqrtf(xnb) * cmaxf + 4.0f * (xnb + cmax2f)) +
+      ebuf[(i & (NE - 1)) * XT + r] = (0x1p-20f * (G::C1 * sqrtf(xnb) * cmaxf + G::C2 * (xnb + cmax2f)) +
                           (8.0f * XD + 32.0f) * 0x1p-53f * (xnb + cmax2f)) * (1.0f + 0x1p-10f);
       }
       fence_proxy_async();
@@ -587,11 +675,11 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
           // the f64 rows of this tile from the stage (landed before the converters ran; the
           // wait only orders this warp's reads after the TMA)
           mbar_sleep(x_full + s, (uint32_t)ph);
-          const unsigned char* xs = sm + L.x0 + s * X_TILE;
-          if (live) {
+          const unsigned char* xs = sm + L.x0 + s * G::X_TILE;
+          if (XD != 32 && live) {  // (XD = 32 reads its row from the stage in the recipe)
 #pragma unroll
             for (int c = 0; c < XD / 2; ++c) {
-              const double2 vv = *reinterpret_cast<const double2*>(xs + swz(r, c));
+              const double2 vv = *reinterpret_cast<const double2*>(xs + xoff<XD>(r, c));
               x[2 * c] = vv.x;
               x[2 * c + 1] = vv.y;
             }
@@ -623,15 +711,21 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
           const int f = __ffs(fl) - 1;
           fl &= fl - 1;
           const int fo = __shfl_sync(0xffffffffu, orig, f);
+          // row f's values from the stage (a shared-memory broadcast), the centroids in place
           double xf[XD];
+          {
+            const unsigned char* xsf = sm + L.x0 + s * G::X_TILE;
 #pragma unroll
-          for (int e = 0; e < XD; ++e) xf[e] = __shfl_sync(0xffffffffu, x[e], f);
+            for (int c = 0; c < XD / 2; ++c) {
+              const double2 vv = *reinterpret_cast<const double2*>(xsf + xoff<XD>(q * 32 + f, c));
+              xf[2 * c] = vv.x;
+              xf[2 * c + 1] = vv.y;
+            }
+          }
           double bd = CUDART_INF;
           int bp = 0x7fffffff, bj = 0;
           for (int j = lane; j < k; j += 32) {
-            double cj[XD];
-            load_crow<XD>(crow, j, cj);
-            const double dj = sqrt(exact_sq_fixed<XD>(xf, cj));
+            const double dj = sqrt(exact_sq_fixed<XD>(xf, crow + j * crow_stride<XD>()));
             const int pj = j == fo ? -1 : j;
             if (dj < bd || (dj == bd && pj < bp)) { bd = dj; bp = pj; bj = j; }
           }
@@ -648,9 +742,13 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
           }
         }
         if (live && cert && !(KNB_TCX_ABL & 4)) {
-          double cw[XD];
-          load_crow<XD>(crow, win, cw);
-          nd = sqrt(exact_sq_fixed<XD>(x, cw));
+          if constexpr (XD == 32) {  // (row and centroid straight from shared memory: registers)
+            nd = sqrt(exact_sq_fixed<XD>(StageRow<XD>{sm + L.x0 + s * G::X_TILE, r}, crow + win * crow_stride<XD>()));
+          } else {
+            double cw[XD];
+            load_crow<XD>(crow, win, cw);
+            nd = sqrt(exact_sq_fixed<XD>(x, cw));
+          }
         }
         const bool moved = live && !queued && win != orig;
         if (live && !queued && !(KNB_TCX_ABL & 8)) {
@@ -734,6 +832,7 @@ constexpr int DW = 8;           // warps per CTA
 
 __host__ __device__ inline int delta_chunk(int k) { return k <= 112 ? 256 : 128; }
 
+template <int XD>
 size_t delta_smem(int k) {
   return (size_t)DW * k * (XD + 2) * sizeof(double)   // private sums
          + (size_t)DW * 2 * 32 * XD * sizeof(double)  // staging rows
@@ -743,8 +842,12 @@ size_t delta_smem(int k) {
 }
 
 // staging offset (doubles) of element e of row rr: 16-byte chunks swizzled by the row
-__device__ __forceinline__ int sw_off(int rr, int e) { return rr * XD + ((((e >> 1) ^ rr) & 7) << 1) + (e & 1); }
+template <int XD>
+__device__ __forceinline__ int sw_off(int rr, int e) {
+  return rr * XD + ((((e >> 1) ^ rr) & (XD / 2 - 1)) << 1) + (e & 1);
+}
 
+template <int XD>
 __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArgs a) {
   pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -828,14 +931,16 @@ __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArg
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(id + 4),
                      "l"(a.recs + (size_t)t * TC_REC + 16 + (r & ~3)) : "memory");
       }
-      // eight lanes per row: lane l copies 16-byte chunk l & 7 of row 4 i + l / 8
+      // XD / 2 lanes per row: lane l copies 16-byte chunk l % (XD / 2) of row
+      // (64 / XD) i + l / (XD / 2): whole rows per instruction
+      constexpr int CPR = XD / 2, RPI = 32 / CPR;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = 4 * i + (lane >> 3);
+      for (int i = 0; i < 32 / RPI; ++i) {
+        const int rr = RPI * i + lane / CPR;
         const long long rw = __shfl_sync(0xffffffffu, row, rr);
         if (rr < n)
-          cp_async16_s(stg_s + (uint32_t)((sl * 32 * XD + sw_off(rr, 2 * (lane & 7))) * sizeof(double)),
-                       a.X + rw * XD + 2 * (lane & 7));
+          cp_async16_s(stg_s + (uint32_t)((sl * 32 * XD + sw_off<XD>(rr, 2 * (lane % CPR))) * sizeof(double)),
+                       a.X + rw * XD + 2 * (lane % CPR));
       }
       cp_async_commit();
       return n;
@@ -853,7 +958,7 @@ __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArg
         double x[XD];
 #pragma unroll
         for (int e = 0; e < XD; e += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(sg + sw_off(lane, e));
+          const double2 v = *reinterpret_cast<const double2*>(sg + sw_off<XD>(lane, e));
           x[e] = v.x;
           x[e + 1] = v.y;
         }
@@ -862,42 +967,45 @@ __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArg
         id[lane].y = (v.y >> (8 * sub)) & 0xFF;  // the old id's byte
       }
       __syncwarp();
-      // per lane: the sum it owns is base[cluster * stride] (dims: acc[c][e]; lane 16: cnt[c];
-      // lane 17: sqa[c]; lanes 18-31 a dummy slot) and the value it adds (lane 16: 1).  No
-      // branches: every lane runs the same read-modify-writes.  Two consecutive rows whose
-      // four clusters are distinct (the usual case) are read, added and written together;
-      // otherwise one after the other -- the same order of additions per sum either way.
-      double* base = lane < XD ? acc + lane : (lane == XD ? cnt : (lane == XD + 1 ? sqa : dummy + warp));
-      const int stride = lane < XD ? XD : (lane <= XD + 1 ? 1 : 0);
+      // per lane and pass: the sum it owns is base[cluster * stride] (value vi = 32 pass +
+      // lane: the dims acc[c][vi], then cnt[c], sqa[c]; idle lanes a dummy slot) and the
+      // value it adds (the count's is 1).  No branches: every lane runs the same
+      // read-modify-writes.  Two consecutive rows whose four clusters are distinct (the
+      // usual case) are read, added and written together; otherwise one after the other --
+      // the same order of additions per sum either way.
       const int to_l = id[lane].x, fr_l = id[lane].y;
-      auto val = [&](int j) {
-        return lane < XD ? sg[sw_off(j, lane)] : (lane == XD + 1 ? sq[j] : 1.0);
-      };
-      int j = 0;
-      while (j < n) {
-        const int t0 = __shfl_sync(0xffffffffu, to_l, j), f0 = __shfl_sync(0xffffffffu, fr_l, j);
-        const int j1 = j + 1 < n ? j + 1 : j;
-        const int t1 = __shfl_sync(0xffffffffu, to_l, j1), f1 = __shfl_sync(0xffffffffu, fr_l, j1);
-        if (j + 1 < n && t1 != t0 && t1 != f0 && f1 != t0 && f1 != f0) {
-          const double v0 = val(j), w0 = val(j + 1);
-          double* a0 = base + t0 * stride;
-          double* b0 = base + f0 * stride;
-          double* a1 = base + t1 * stride;
-          double* b1 = base + f1 * stride;
-          const double ra0 = *a0, rb0 = *b0, ra1 = *a1, rb1 = *b1;
-          *a0 = ra0 + v0;
-          *b0 = rb0 - v0;
-          *a1 = ra1 + w0;
-          *b1 = rb1 - w0;
-          j += 2;
-        } else {
-          const double v0 = val(j);
-          double* a0 = base + t0 * stride;
-          double* b0 = base + f0 * stride;
-          const double ra0 = *a0, rb0 = *b0;
-          *a0 = ra0 + v0;
-          *b0 = rb0 - v0;
-          j += 1;
+#pragma unroll
+      for (int pass = 0; pass < (XD + 2 + 31) / 32; ++pass) {
+        const int vi = 32 * pass + lane;
+        double* base = vi < XD ? acc + vi : (vi == XD ? cnt : (vi == XD + 1 ? sqa : dummy + warp));
+        const int stride = vi < XD ? XD : (vi <= XD + 1 ? 1 : 0);
+        auto val = [&](int j) { return vi < XD ? sg[sw_off<XD>(j, vi)] : (vi == XD + 1 ? sq[j] : 1.0); };
+        int j = 0;
+        while (j < n) {
+          const int t0 = __shfl_sync(0xffffffffu, to_l, j), f0 = __shfl_sync(0xffffffffu, fr_l, j);
+          const int j1 = j + 1 < n ? j + 1 : j;
+          const int t1 = __shfl_sync(0xffffffffu, to_l, j1), f1 = __shfl_sync(0xffffffffu, fr_l, j1);
+          if (j + 1 < n && t1 != t0 && t1 != f0 && f1 != t0 && f1 != f0) {
+            const double v0 = val(j), w0 = val(j + 1);
+            double* a0 = base + t0 * stride;
+            double* b0 = base + f0 * stride;
+            double* a1 = base + t1 * stride;
+            double* b1 = base + f1 * stride;
+            const double ra0 = *a0, rb0 = *b0, ra1 = *a1, rb1 = *b1;
+            *a0 = ra0 + v0;
+            *b0 = rb0 - v0;
+            *a1 = ra1 + w0;
+            *b1 = rb1 - w0;
+            j += 2;
+          } else {
+            const double v0 = val(j);
+            double* a0 = base + t0 * stride;
+            double* b0 = base + f0 * stride;
+            const double ra0 = *a0, rb0 = *b0;
+            *a0 = ra0 + v0;
+            *b0 = rb0 - v0;
+            j += 1;
+          }
         }
       }
       __syncwarp();
@@ -928,6 +1036,7 @@ __global__ void __launch_bounds__(DW * 32, 1) mti_tc_delta_kernel(const MtiTcArg
 // the current centroid on an exact tie and otherwise the lowest id (pruning.py:174-203).
 // Then the row's MTI state, and for a moved row its bit and old id in the tile's record
 // (the epilogue left both out), so mti_tc_delta_kernel sums it like any other moved row.
+template <int XD>
 __global__ void __launch_bounds__(256) mti_tc_rerank_kernel(const MtiTcArgs a) {
   pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -1031,26 +1140,42 @@ __global__ void __launch_bounds__(256) mti_tc_rerank_kernel(const MtiTcArgs a) {
   }
 }
 
-// B operand image in global memory, exactly as the kernel's shared memory holds it:
-// chunk 0 row j = [-2 c_hi | -2 c_hi], chunk 1 row j = [-2 c_lo | cn2_hi, cn2_lo, 1, 1,
-// 0, 0, 0, 0 | 0 ...]; padded rows j >= k score 2^100 (never a winner, never in a window)
+// B operand image in global memory, exactly as the kernel's shared memory holds it (Geo's
+// layout for XD; the cn2 entries carry ||c_j||^2 as hi + lo, the A side's [1, 1] picks
+// them up); padded rows j >= k score 2^100 (never a winner, never in a window)
+template <int XD>
 __global__ void mti_tc_prep_kernel(const double* __restrict__ means, int k, int N, uint4* __restrict__ bimg,
                                    unsigned long long* __restrict__ rq_count) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && rq_count) *rq_count = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * N * 8; i += gridDim.x * blockDim.x) {
+  constexpr int NCH = Geo<XD>::B_NCH;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NCH * N * 8; i += gridDim.x * blockDim.x) {
     const int chunk = i / (N * 8), rem = i - chunk * N * 8, j = rem >> 3, qq = rem & 7;
     float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     const bool real = j < k;
-    if (chunk == 0 || qq < 4) {
-      const int e0 = (chunk == 0 ? (qq & 3) : qq) * 4;
+    // what 16-byte chunk (chunk, qq) of row j holds: -2 c_hi / -2 c_lo at dims e0.., or the
+    // norm constants, or zeros
+    int kind = 0, e0 = 0;  // 1: c_hi, 2: c_lo, 3: constants
+    if constexpr (XD == 8) {
+      if (qq < 4) { kind = 1; e0 = (qq & 1) * 4; }
+      else if (qq < 6) { kind = 2; e0 = (qq - 4) * 4; }
+      else if (qq == 6) kind = 3;
+    } else if constexpr (XD == 16) {
+      if (chunk == 0) { kind = 1; e0 = (qq & 3) * 4; }
+      else if (qq < 4) { kind = 2; e0 = qq * 4; }
+      else if (qq == 4) kind = 3;
+    } else {
+      if (chunk < 2) { kind = chunk + 1; e0 = qq * 4; }
+      else if (qq == 0) kind = 3;
+    }
+    if (kind == 1 || kind == 2) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const double c = real ? means[(long long)j * XD + e0 + m] : 0.0;
         const float ch = tf32_trunc(__double2float_rn(c));
         const float cl = tf32_rna(__double2float_rn(c - (double)ch));
-        v[m] = -2.0f * (chunk == 0 ? ch : cl);
+        v[m] = -2.0f * (kind == 1 ? ch : cl);
       }
-    } else if (qq == 4) {
+    } else if (kind == 3) {
       double cn2 = 0.0;
       if (real)
         for (int e = 0; e < XD; ++e) {
@@ -1070,36 +1195,70 @@ __global__ void mti_tc_prep_kernel(const double* __restrict__ means, int k, int 
   }
 }
 
-template <int NG, int LAST>
+template <int XD, int NG, int LAST>
 cudaError_t launch_ng(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s) {
-  const TcxSmem L(a.k, 16 * NG, a.nx);
+  const TcxSmem<XD> L(a.k, 16 * NG, a.nx);
   cudaError_t e =
-      cudaFuncSetAttribute(mti_tc_kernel<NG, LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      cudaFuncSetAttribute(mti_tc_kernel<XD, NG, LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  return launch_pdl(mti_tc_kernel<NG, LAST>, dim3(grid), dim3(THREADS), L.total, s, *tm, a);
+  return launch_pdl(mti_tc_kernel<XD, NG, LAST>, dim3(grid), dim3(THREADS), L.total, s, *tm, a);
 }
 
-template <int NG>
+template <int XD, int NG>
 cudaError_t launch_last(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s) {
   // the score dump reads every column; otherwise the last group reads 8 when that covers k
-  if (!a.dbg && a.k <= 16 * (NG - 1) + 8) return launch_ng<NG, 8>(tm, a, grid, s);
-  return launch_ng<NG, 16>(tm, a, grid, s);
+  if (!a.dbg && a.k <= 16 * (NG - 1) + 8) return launch_ng<XD, NG, 8>(tm, a, grid, s);
+  return launch_ng<XD, NG, 16>(tm, a, grid, s);
+}
+
+template <int XD>
+cudaError_t launch_xd(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s) {
+  switch ((a.k + 15) / 16) {
+    case 1: return launch_last<XD, 1>(tm, a, grid, s);
+    case 2: return launch_last<XD, 2>(tm, a, grid, s);
+    case 3: return launch_last<XD, 3>(tm, a, grid, s);
+    default: break;
+  }
+  if constexpr (XD != 32) {  // (row width 32: k <= 32, see mti_tc_stages)
+    switch ((a.k + 15) / 16) {
+      case 4: return launch_last<XD, 4>(tm, a, grid, s);
+      case 5: return launch_last<XD, 5>(tm, a, grid, s);
+      case 6: return launch_last<XD, 6>(tm, a, grid, s);
+      case 7: return launch_last<XD, 7>(tm, a, grid, s);
+      case 8: return launch_last<XD, 8>(tm, a, grid, s);
+      default: break;
+    }
+  }
+  return cudaErrorInvalidValue;
 }
 
 constexpr size_t SMEM_MAX = 227 * 1024;
 
-}  // namespace
-
-// stages of the f64 ring that fit (0: the kernel does not apply)
-int mti_tc_stages(int d, int k) {
-  if (d != XD || k < 1 || k > 128) return 0;
+template <int XD>
+int stages_xd(int k) {
   const int N = (k + 15) / 16 * 16;
-  for (int nx = KNB_TCX_NXMAX; nx >= 2; --nx)
-    if (TcxSmem(k, N, nx).total <= SMEM_MAX) return nx;
+  if (delta_smem<XD>(k) > SMEM_MAX) return 0;
+  for (int nx = KNB_TCX_NXMAX; nx >= 3; --nx)
+    if (TcxSmem<XD>(k, N, nx).total <= SMEM_MAX) return nx;
   return 0;
 }
 
-size_t mti_tc_bimg_bytes(int k) { return (size_t)2 * ((k + 15) / 16 * 16) * 128; }
+}  // namespace
+
+// stages of the f64 ring that fit (0: the kernel does not apply): rows of 8, 16 or 32
+// doubles, k <= 128 (row width 32: k <= 32, the delta kernel's staging and sums)
+int mti_tc_stages(int d, int k) {
+  if (k < 1 || k > 128) return 0;
+  if (d == 8) return stages_xd<8>(k);
+  if (d == 16) return stages_xd<16>(k);
+  if (d == 32) return k <= 32 ? stages_xd<32>(k) : 0;
+  return 0;
+}
+
+size_t mti_tc_bimg_bytes(int d, int k) {
+  const int nch = d == 32 ? 3 : (d == 16 ? 2 : 1);
+  return (size_t)nch * ((k + 15) / 16 * 16) * 128;
+}
 
 int mti_tc_prof(unsigned long long* out) {
   unsigned long long all[18];
@@ -1111,38 +1270,50 @@ int mti_tc_prof(unsigned long long* out) {
   return KNB_TCX_PROF;
 }
 
-cudaError_t launch_mti_tc_prep(const double* means, int k, void* bimg, unsigned long long* rq_count, cudaStream_t s) {
+cudaError_t launch_mti_tc_prep(const double* means, int d, int k, void* bimg, unsigned long long* rq_count,
+                               cudaStream_t s) {
   const int N = (k + 15) / 16 * 16;
-  mti_tc_prep_kernel<<<(2 * N * 8 + 255) / 256, 256, 0, s>>>(means, k, N, reinterpret_cast<uint4*>(bimg), rq_count);
+  const int blocks = (3 * N * 8 + 255) / 256;
+  uint4* b = reinterpret_cast<uint4*>(bimg);
+  if (d == 8) mti_tc_prep_kernel<8><<<blocks, 256, 0, s>>>(means, k, N, b, rq_count);
+  else if (d == 16) mti_tc_prep_kernel<16><<<blocks, 256, 0, s>>>(means, k, N, b, rq_count);
+  else mti_tc_prep_kernel<32><<<blocks, 256, 0, s>>>(means, k, N, b, rq_count);
   return cudaGetLastError();
 }
 
-cudaError_t launch_mti_tc_rerank(const MtiTcArgs& a, int grid, cudaStream_t s) {
+template <int XD>
+cudaError_t rerank_xd(const MtiTcArgs& a, int grid, cudaStream_t s) {
   const size_t smem = (size_t)a.k * crow_stride<XD>() * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(mti_tc_rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(mti_tc_rerank_kernel<XD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(mti_tc_rerank_kernel, dim3(grid), dim3(256), smem, s, a);
+  return launch_pdl(mti_tc_rerank_kernel<XD>, dim3(grid), dim3(256), smem, s, a);
+}
+
+cudaError_t launch_mti_tc_rerank(const MtiTcArgs& a, int grid, cudaStream_t s) {
+  if (a.d == 8) return rerank_xd<8>(a, grid, s);
+  if (a.d == 16) return rerank_xd<16>(a, grid, s);
+  return rerank_xd<32>(a, grid, s);
+}
+
+template <int XD>
+cudaError_t delta_xd(const MtiTcArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = delta_smem<XD>(a.k);
+  cudaError_t e = cudaFuncSetAttribute(mti_tc_delta_kernel<XD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(mti_tc_delta_kernel<XD>, dim3(grid), dim3(DW * 32), smem, s, a);
 }
 
 cudaError_t launch_mti_tc_delta(const MtiTcArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = delta_smem(a.k);
-  cudaError_t e = cudaFuncSetAttribute(mti_tc_delta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(mti_tc_delta_kernel, dim3(grid), dim3(DW * 32), smem, s, a);
+  if (a.d == 8) return delta_xd<8>(a, grid, s);
+  if (a.d == 16) return delta_xd<16>(a, grid, s);
+  return delta_xd<32>(a, grid, s);
 }
 
 cudaError_t launch_mti_tc(const CUtensorMap* tm, const MtiTcArgs& a, int grid, cudaStream_t s) {
-  switch ((a.k + 15) / 16) {
-    case 1: return launch_last<1>(tm, a, grid, s);
-    case 2: return launch_last<2>(tm, a, grid, s);
-    case 3: return launch_last<3>(tm, a, grid, s);
-    case 4: return launch_last<4>(tm, a, grid, s);
-    case 5: return launch_last<5>(tm, a, grid, s);
-    case 6: return launch_last<6>(tm, a, grid, s);
-    case 7: return launch_last<7>(tm, a, grid, s);
-    case 8: return launch_last<8>(tm, a, grid, s);
-    default: return cudaErrorInvalidValue;
-  }
+  if (a.d == 8) return launch_xd<8>(tm, a, grid, s);
+  if (a.d == 16) return launch_xd<16>(tm, a, grid, s);
+  if (a.d == 32) return launch_xd<32>(tm, a, grid, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace knb

@@ -20,7 +20,7 @@ struct Ctrl {
   int max_iters;
   double tolerance;      // reassigned <= tolerance converges
   int mti_choice;        // next pruned pass: 1 = block-dense (few skips), 0 = compacted survivors
-  int pad_;
+  int block_pct;         // the block (or tcgen05) pass runs while clause 1 skips < block_pct % of rows
   double cmax2;          // max_j ||c_j||^2 of the current means (dense certificate)
   long long count_seen;  // last Sigma counts
 };

@@ -197,7 +197,7 @@ __device__ void stats_body(const FinalArgs& f) {
     // adaptive MTI kernel for the next pass: streaming every block only beats
     // compacting the survivors when clause 1 skips almost nothing (measured: c2 with
     // 49% skips 0.46 vs 0.28 ms, c4 with 0% skips 183 vs 190 ms)
-    c->mti_choice = (double)st.skips < 0.10 * (double)f.n ? 1 : 0;
+    c->mti_choice = (double)st.skips < 0.01 * c->block_pct * (double)f.n ? 1 : 0;
     c->cmax2 = M;
     c->full_pass = 0;
     c->t = t + 1;
