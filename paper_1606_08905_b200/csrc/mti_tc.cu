@@ -230,10 +230,27 @@ __device__ __forceinline__ float tf32_rna(float v) {
 #ifndef KNB_TCX_SPIN
 #define KNB_TCX_SPIN 0
 #endif
+#ifndef KNB_TCX_BACKOFF
+#define KNB_TCX_BACKOFF 0
+#endif
 __device__ __forceinline__ void mbar_sleep(uint64_t* bar, uint32_t parity) {
   if (KNB_TCX_SPIN) {
     mbar_wait(bar, parity);
     return;
+  }
+  if (KNB_TCX_BACKOFF > 0) {  // poll, then sleep a fixed time between polls
+    uint32_t ok;
+    for (;;) {
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, P1;\n\t}"
+          : "=r"(ok)
+          : "r"(smem_u32(bar)), "r"(parity)
+          : "memory");
+      if (ok) return;
+      __nanosleep(KNB_TCX_BACKOFF);
+    }
   }
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -469,8 +486,6 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
   } else if (warp < W_EPI) {
     // ------------------------------------------------------------ converters
     const int r0 = (warp - W_CONV) * 32 + lane;
-    const float cmaxf = __double2float_ru(sqrt(a.ctrl->cmax2));
-    const float cmax2f = __double2float_ru(a.ctrl->cmax2);
     ProfClock pc;
     pc.start();
     int s = 0, ph = 0;
@@ -540,11 +555,9 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
         put(AC, q0, 1.0f, 1.0f, xh, xl);
         put(AC, q0 + 1, 0.0f, 0.0f, 0.0f, 0.0f);
       }
-      // the certificate's bound E(x) for the epilogue (f32 with a relative margin;
-      // xn2 carries < 2^-20 relative error)
-      const float xnb = xn2 * (1.0f + 0x1p-12f);
-      ebuf[(i & (NE - 1)) * XT + r] = (0x1p-20f * (G::C1 * sqrtf(xnb) * cmaxf + G::C2 * (xnb + cmax2f)) +
-                          (8.0f * XD + 32.0f) * 0x1p-53f * (xnb + cmax2f)) * (1.0f + 0x1p-10f);
+      // ||x||^2 for the epilogue's certificate bound E(x) (with a relative margin: xn2
+      // carries < 2^-20 relative error)
+      ebuf[(i & (NE - 1)) * XT + r] = xn2 * (1.0f + 0x1p-12f);
       }
       fence_proxy_async();
       __syncwarp();
@@ -562,6 +575,8 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
     const int q = warp & 3;          // TMEM lane quarter
     const int r = q * 32 + lane;     // row within the tile
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    const float cmaxf = __double2float_ru(sqrt(a.ctrl->cmax2));
+    const float cmax2f = __double2float_ru(a.ctrl->cmax2);
     auto state = [&](int i, int& av, double& uv) {
       const long long row = (long long)(t0 + i * tstep) * XT + r;
       const bool ok = i < mine && row < a.n;
@@ -665,7 +680,10 @@ __global__ void __maxnreg__(KNB_TCX_REGS)
       if (!a.dbg && lmask && !(KNB_TCX_ABL & 2)) {
         bool cert = false;
         if (live) {
-          const float E = ebuf[(i & (NE - 1)) * XT + r];
+          // the certificate's bound E(x) (f32 with a relative margin)
+          const float xnb = ebuf[(i & (NE - 1)) * XT + r];
+          const float E = (0x1p-20f * (G::C1 * sqrtf(xnb) * cmaxf + G::C2 * (xnb + cmax2f)) +
+                           (8.0f * XD + 32.0f) * 0x1p-53f * (xnb + cmax2f)) * (1.0f + 0x1p-10f);
           const float m1 = __int_as_float(k1 & ~127), m2 = __int_as_float(k2 & ~127);
           // key slack (< 2^-16 relative each) and the f32 rounding of this test
           cert = (m2 - m1) > 2.0f * E + 0x1p-15f * (fabsf(m1) + fabsf(m2)) && win < k;
