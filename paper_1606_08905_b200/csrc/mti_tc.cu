@@ -1,6 +1,7 @@
-// K6/K7-TC: the pruned (MTI) pass for f64 rows with d = 16 on the tcgen05 tensor
-// cores, with a certified argmin (BASELINE config 4: n = 856M, d = 16, k = 100,
-// where clause 1 skips almost nothing and every row is re-scored each pass).
+// K6/K7-TC: the pruned (MTI) pass for f64 rows on the tcgen05 tensor cores, with a
+// certified argmin.  Rows of 16 doubles take it automatically (BASELINE config 4: n =
+// 856M, d = 16, k = 100, where clause 1 skips almost nothing and every row is re-scored
+// each pass); rows of 8 and 32 (configs 3, 2) run it when forced (mti_scan="tc").
 //
 // Replaces numakmeans engine._task_pruned (engine.py:321-354) + inflate_bounds
 // (pruning.py:152-160) + scan_block (pruning.py:163-204) with the semantics of the
@@ -14,48 +15,48 @@
 // Scores.  The tensor core has no f64 kind, and DMMA (mma.sync f64) runs the c4 pass
 // at ~0.5 of the FP64 peak (latency bound, 8 warps).  Here each f64 value is split
 // into two TF32 terms -- x = x_hi + x_lo (x_hi = f32(x) truncated to 10 mantissa bits,
-// x_lo the f32 remainder, truncated by the tensor core) -- and one chain of seven
-// kind::tf32 UMMAs (M = 128 rows, N = k padded to 16, K = 8 each) accumulates, in
-// TMEM,
+// x_lo the f32 remainder, truncated by the tensor core) -- and one chain of kind::tf32
+// UMMAs (M = 128 rows, N = k padded to 16, K = 8 each: 4 / 7 / 13 of them for rows of
+// 8 / 16 / 32, Geo<XD>) accumulates, in TMEM,
 //     D~_j = (x_hi + x_lo).(-2 c_hi)  +  x_hi.(-2 c_lo)  +  ||c_j||^2  +  ||x||^2
 //          ~ ||x - c_j||^2
 // (the x_lo.c_lo term, ~2^-20 |x||c|, is dropped; the two norms enter through a
-// constant k-step: A = [1, 1, xn2_hi, xn2_lo], B = [cn2_hi, cn2_lo, 1, 1]).
-// Operand layout, K-major with the 128-byte swizzle (tc_common.cuh descriptors):
-//     A chunk 0 = [x_hi(16) | x_lo(16)]      B chunk 0 = [-2c_hi(16) | -2c_hi(16)]
-//     A chunk 1 = [x_hi(16) | consts(8)]     B chunk 1 = [-2c_lo(16) | consts(8)]
-// k-steps 0-3 on chunk 0, 0-2 on chunk 1.
+// constant k-step: A = [1, 1, xn2_hi, xn2_lo], B = [cn2_hi, cn2_lo, 1, 1]); the operand
+// layouts are listed at Geo.
 //
 // Certificate.  |D~_j - D_j| <= E(x) with
-//     E = 2^-20 (12 ||x|| cmax + 4 (||x||^2 + cmax^2)) + (8d + 32) 2^-53 (||x||^2 + cmax^2)
-// (operand splitting: <= 3.2 * 2^-20 |x_i c_i| per product, x2 for the -2 scale; the
-// f32 accumulation over seven k-steps: <= 2^-22 per step of the partial magnitudes,
-// bounded by ||x||^2 + cmax^2 + 2 ||x|| cmax; the last term is the reference's own f64
-// rounding of sum (x - c)^2, as in the DMMA certificate).  tests/test_gpu_mti_tc.py
-// measures the worst |D~ - D| / E on adversarial inputs and requires < 1/4.
-// The epilogue finds the smallest and second-smallest D~ of the row with integer
-// min trees on keys = (f32 bits & ~127) | column (order-preserving for D~ >= 0; the
-// column index rides in the low 7 bits, < 2^-16 relative); a row is CERTIFIED when
-// second - first > 2E (+ the key slack): its winner is the reference's argmin.  Other
-// rows (near ties, exact ties, tiny negative D~) are re-ranked by the whole warp with
-// the exact recipe over all k centroids in scan_block's order (current centroid
-// first, strict <), so the outputs are the reference's bit for bit.
+//     E = 2^-20 (C1 ||x|| cmax + C2 (||x||^2 + cmax^2)) + (8d + 32) 2^-53 (||x||^2 + cmax^2)
+// (C1 = 12.5, C2 = 4 for rows of 8 / 16, 20 and 6 for 32: operand splitting <= 3.2 *
+// 2^-20 |x_i c_i| per product, x2 for the -2 scale; the f32 accumulation <= 2^-22 per
+// k-step of the partial magnitudes, bounded by ||x||^2 + cmax^2 + 2 ||x|| cmax; the
+// last term is the reference's own f64 rounding of sum (x - c)^2, as in the DMMA
+// certificate).  tests/test_gpu_mti_tc.py measures the worst |D~ - D| / E on
+// adversarial inputs of every width and requires < 1/4.  The epilogue finds the
+// smallest and second-smallest D~ of the row with integer min trees on keys = (f32 bits
+// & ~127) | column (order-preserving for D~ >= 0; the column index rides in the low 7
+// bits, < 2^-16 relative); a row is CERTIFIED when second - first > 2E (+ the key
+// slack): its winner is the reference's argmin.  Other rows (near ties, exact ties,
+// tiny negative D~) go to a queue that mti_tc_rerank_kernel re-ranks after the pass
+// with the exact recipe in scan_block's order (current centroid first, strict <);
+// beyond the queue's capacity the warp re-ranks them in the pass.  The outputs are the
+// reference's bit for bit.
 //
 // Kernel shape (one CTA per SM, persistent over 128-row tiles, static schedule):
-//   warp 0      TMA producer: f64 row tiles (128 rows x 128 B, SWIZZLE_128B) through an
+//   warp 0      TMA producer: f64 row tiles (128 rows, SWIZZLE_128B / 64B) through an
 //               NX-stage ring, tiles PF ahead prefetched into L2
-//   warp 1      TMEM allocation (NGRP x 128 columns: one accumulator per epilogue group)
-//               and the single-thread UMMA issuer
-//   warps 2-3   converters (NCONV): f64 -> (x_hi, x_lo) TF32 operand tile (two 128-byte
-//               chunks) + the norm constants + E(x) per row, NA-stage ring
-//   NGRP groups of four epilogue warps, tile i on group i % NGRP: one thread per row
-//               (TMEM lane), key min trees, certificate, warp-wide exact rerank of
-//               uncertified rows, exact bound of the winner from the f64 tile, MTI
+//   warp 1      TMEM allocation (four 128-column accumulators) and the single-thread
+//               UMMA issuer (tile i into accumulator i % 4)
+//   warps 2-3   converters (NCONV): f64 -> (x_hi, x_lo) TF32 operand tile + the norm
+//               constants + ||x||^2 per row, NA-stage ring
+//   NGRP = 3 groups of four epilogue warps, tile i on group i % 3: one thread per row
+//               (TMEM lane), key min trees, certificate (E(x) from ||x||^2), queue of
+//               uncertified rows, exact bound of the winner from the f64 stage, MTI
 //               state; then the f64 stage is released and the tile's moved rows are
 //               written as a 144-byte record (row mask + old ids)
+// mti_tc_rerank_kernel settles the queued rows (and adds their records' moved bits);
 // mti_tc_delta_kernel turns the records into per-CTA signed deltas of sums / counts /
 // sq in row order (deterministic), summed by reduce_kernel like every other pass.
-// HBM traffic per row: 128 B of rows + 13 B of state read + 13 B written (+ records).
+// HBM traffic per row: 8d B of rows + 13 B of state read + 9-13 B written (+ records).
 #include <cuda.h>
 #include <math_constants.h>
 
@@ -88,7 +89,6 @@ struct Geo {
   static_assert(XD == 8 || XD == 16 || XD == 32, "row widths 8, 16, 32");
   static constexpr uint32_t X_TILE = XT * XD * 8;         // f64 stage bytes
   static constexpr int NTMA = XD == 32 ? 2 : 1;           // TMA boxes per tile
-  static constexpr int BOXW = XD == 8 ? 8 : 16;           // box width (doubles)
   static constexpr int A_NCH = XD == 32 ? 3 : (XD == 16 ? 2 : 1);  // operand chunks (incl. constants)
   static constexpr uint32_t A_TILE = A_NCH * CH;
   static constexpr int B_NCH = A_NCH;
@@ -201,21 +201,6 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[16]) {
   }
 }
 
-// K-major no-swizzle operand (8-row x 16-byte core matrices): byte offset of 16-byte
-// chunk c of row r with K-adjacent core matrices 128 B apart and 8-row groups 256 B apart
-__device__ __forceinline__ uint32_t plain_off(int r, int c) {
-  return (uint32_t)(r >> 3) * 256u + (uint32_t)c * 128u + (uint32_t)(r & 7) * 16u;
-}
-// its shared-memory descriptor (layout type 0 = no swizzle; LBO along K, SBO along M/N)
-__device__ __forceinline__ uint64_t umma_desc_plain(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1u << 46;
-  return d;
-}
-
 __device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
 __device__ __forceinline__ float tf32_rna(float v) {
@@ -230,27 +215,10 @@ __device__ __forceinline__ float tf32_rna(float v) {
 #ifndef KNB_TCX_SPIN
 #define KNB_TCX_SPIN 0
 #endif
-#ifndef KNB_TCX_BACKOFF
-#define KNB_TCX_BACKOFF 0
-#endif
 __device__ __forceinline__ void mbar_sleep(uint64_t* bar, uint32_t parity) {
   if (KNB_TCX_SPIN) {
     mbar_wait(bar, parity);
     return;
-  }
-  if (KNB_TCX_BACKOFF > 0) {  // poll, then sleep a fixed time between polls
-    uint32_t ok;
-    for (;;) {
-      asm volatile(
-          "{\n\t.reg .pred P1;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-          "selp.u32 %0, 1, 0, P1;\n\t}"
-          : "=r"(ok)
-          : "r"(smem_u32(bar)), "r"(parity)
-          : "memory");
-      if (ok) return;
-      __nanosleep(KNB_TCX_BACKOFF);
-    }
   }
   asm volatile(
       "{\n\t.reg .pred P1;\n"
