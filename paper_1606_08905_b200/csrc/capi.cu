@@ -234,8 +234,6 @@ FinalArgs final_args(knb_ctx* c) {
 }
 
 // fresh run state: iteration 0, not stopped, assignment zero, running sums zero
-bool tcx_ready(const knb_ctx* c);
-
 int reset_run(knb_ctx* c) {
   Ctrl h;
   std::memset(&h, 0, sizeof(h));
