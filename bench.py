@@ -232,6 +232,8 @@ def run_ours(args):
     force_comm = os.environ.get("KNB_BENCH_FORCE_COMM") == "1"  # NCCL step loop even at N = 1
     if world > 1 or force_comm:
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # (force_comm without torchrun: a one-rank group)
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29533")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         comm = TorchComm()
     name = args.config
