@@ -16,13 +16,16 @@ total n (strong scaling); c1 / c2 keep n rows per GPU (weak scaling, see WEAK).
 
 Other keys: roofline (the step's dominant kernel, north-star definition:
 dense-equivalent n*k*d FMAs vs point bytes), roofline_k1 (the dense assign
-kernel timed on full passes), cpu_baseline (the oracle port of the reference
-on this host's cores, bounded sample), e2e (full kmeans() public-API calls from
+kernel timed on full passes), cpu_baseline (the reference package, or the oracle port
+when it is not installed, on this host's cores, bounded sample), e2e (full kmeans() public-API calls from
 host numpy arrays, H2D/D2H included), clocks (nvidia-smi during the run).
 
---impl reference times the reference algorithm's CPU implementation (the
-oracle port in oracle/, pinned bit-for-bit to the reference package) on this
-host with all cores, on a bounded row sample of the same workload.
+--impl reference times the reference's own CPU implementation on this host with
+all cores, on a bounded row sample of the same workload: the unmodified
+numakmeans package from baseline/_ref (installed by __graft_entry__.build() in the
+container that holds /root/reference; git-ignored, it travels with the snapshot;
+kind "reference"), else the oracle port in oracle/ (pinned bit-for-bit to the
+reference package; kind "port").
 """
 
 from __future__ import annotations
@@ -182,19 +185,56 @@ def cpu_port_run(name, cfg, n_sub, iters, threads):
     return [s.wall_s for s in r.iterations], r
 
 
-def cpu_baseline(name, cfg, warmup, steps):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_pkg():
+    """The unmodified numakmeans package as build() installed it into baseline/_ref
+    (git-ignored; it travels to the GPU box with the snapshot), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "numakmeans")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import numakmeans
+        return numakmeans
+    except Exception:
+        return None
+
+
+def cpu_reference_run(nk, name, cfg, n_sub, iters, threads):
+    """numakmeans.kmeans itself (engine.py:489-500) on n_sub rows; per-iteration wall times.
+    The reference has no forced-iteration mode: a run that converges before `iters` gives
+    fewer samples."""
+    m = cfg["data"](n_sub)
+    if m.dtype != np.float64:
+        m = m.astype(np.float64)
+    ec = nk.EngineConfig(k=cfg["k"], init=cfg["init"], seed=int(name[1:]), pruning=cfg["pruning"],
+                         tolerance=cfg["tolerance"], max_iters=iters, T=threads)
+    r = nk.kmeans(m, ec)
+    return [s.wall_s for s in r.iterations], r
+
+
+def cpu_baseline(name, cfg, warmup, steps, prefer_reference=True):
     n_sub = min(CPU_SAMPLE[name], cfg["n"])
     threads = os.cpu_count() or 1
-    walls, r = cpu_port_run(name, cfg, n_sub, warmup + steps, threads)
+    nk = reference_pkg() if prefer_reference else None
+    if nk is not None:
+        walls, r = cpu_reference_run(nk, name, cfg, n_sub, warmup + steps, threads)
+        kind, what = "reference", "numakmeans.kmeans (the unmodified reference package from baseline/_ref)"
+    else:
+        walls, r = cpu_port_run(name, cfg, n_sub, warmup + steps, threads)
+        kind, what = "port", "oracle/lloyd.py (restatement pinned bit-exact to numakmeans)"
     timed = walls[warmup:warmup + steps] or walls
     value = n_sub * len(timed) / sum(timed)
     rows = (f"the first {n_sub} rows of the {name} stream (default_rng(4).random is prefix-consistent)"
             if name == "c4" else
             f"{n_sub} rows drawn from the {name} law with its seed (a sub-scale instance: the mixtures "
             f"draw labels before noise, so they are not prefix-consistent)")
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle/lloyd.py (restatement pinned bit-exact to numakmeans) on {rows}, its own "
-                      f"{cfg['init']} init, iterations {warmup}..{warmup + len(timed) - 1}, {threads} threads"}
+    first = min(warmup, len(walls) - len(timed))
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{what} on {rows}, its own {cfg['init']} init, iterations "
+                      f"{first}..{first + len(timed) - 1}, {threads} threads"}
 
 
 def run_reference(args):

@@ -23,5 +23,5 @@ def test_reference_arm_json_line():
         assert key in rec, key
     assert rec["impl"] == "reference" and rec["value"] > 0 and rec["higher_is_better"] is True
     assert rec["config"]["workload"] == "c1"
-    assert rec["cpu_baseline"]["kind"] == "port" and rec["cpu_baseline"]["cores"] >= 1
+    assert rec["cpu_baseline"]["kind"] in ("reference", "port") and rec["cpu_baseline"]["cores"] >= 1
     assert rec["e2e"]["h2d_bytes_per_step"] == 0 and rec["e2e"]["value"] == rec["value"]
