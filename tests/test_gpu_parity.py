@@ -369,3 +369,27 @@ def test_gpu_large_common_offset_matches_oracle(pruning):
                   what=f"offset pruning={pruning}")
     # and in units of the spread, not of the 1e8 offset
     assert float(np.abs(r.centroids.means - o.means).max()) < 1e-6
+
+
+@pytest.mark.parametrize("mode", ["auto", "dense", "block", "exact"])
+def test_skewed_row_order_matches_oracle(mode):
+    """SURVEY 8(f) f4 / reference test_engine.py:71-89 (results do not depend on the
+    scheduling policy): rows sorted by their first-pass cluster, so the clause-1 survivors
+    arrive in long contiguous runs and whole row ranges are skipped.  The compacted MTI
+    pass deals 32-row blocks round-robin over the grid; every output equals the oracle's
+    on the same (sorted) rows, and the assignments are the generated-order run's permuted."""
+    m = kb.synth.mixture(kb.synth.MixtureSpec(60_000, 16, 20, 31, "uniform", -5, 5, 0.6, 1.0))
+    first = O.lloyd(m, 20, init="forgy", seed=3, pruning=True, max_iters=1)
+    order = np.argsort(first.assignments, kind="stable")
+    ms = np.ascontiguousarray(m[order])
+    init = first.prev_means
+    cfg = kb.EngineConfig(k=20, init="given", initial_centroids=init, pruning=True, max_iters=30, mti_scan=mode)
+    got = kb.kmeans(ms, cfg)
+    want = O.lloyd(ms, 20, init="given", initial=init, pruning=True, max_iters=30)
+    assert got.n_iterations == want.n_iterations
+    assert np.array_equal(got.assignments, want.assignments)
+    for a, b in zip(got.iterations, want.iterations):
+        assert (a.reassignments, a.skips) == (b.reassignments, b.skips)
+    assert max(s.skips for s in got.iterations) > 0.25 * ms.shape[0]  # long skipped runs did occur
+    plain = kb.kmeans(m, cfg)
+    assert np.array_equal(plain.assignments[order], got.assignments)
