@@ -334,6 +334,71 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
   return nd;
 }
 
+// scan_block's choice for the lane's row by the exact recipe alone, no tensor-core scores
+// (narrow rows and few centroids -- config 3, d = 8, k = 10 -- where k exact distances
+// are ~16 k FP64 instructions and the DMMA scorer's fixed epilogue / combine / certificate
+// cost more): start from the current centroid `orig`, then ascending ids, switch on strict
+// < (pruning.py:174-203).  The scan runs on the SQUARED distances and takes one square
+// root, of the winner: sqrt is monotone, so no switch where sq_j >= best is the
+// reference's decision too, and a switch with sq_j < best (1 - 2^-50) is strict after the
+// roots' roundings (2^-53 relative each); a switch inside that margin -- the roots may
+// collide -- sends the row through the sqrt-domain scan.  Every lane reads the same
+// centroid (shared-memory broadcast).  Returns the winner's distance; id = the winner.
+// FULL: d == DP, the tree's shape is known at compile time (decided once, outside the scan)
+template <int DP, bool FULL>
+__device__ __forceinline__ double direct_scan(const double (&x)[DP], const double* crow, int k, int d, int orig,
+                                              int& id) {
+  auto sqd = [&](int j) {
+    double cj[DP];
+    load_crow<DP>(crow, j, cj);
+    if constexpr (FULL) return exact_sq_fixed<DP>(x, cj);
+    else return exact_sq<DP>(x, cj, d);
+  };
+  double bs = sqd(orig);
+  int bi = orig;
+  bool close = false;
+  // branch-free (selects), two centroids' distance chains in flight
+  auto step = [&](double sj, int j) {  // (j == orig repeats bs bit for bit: no switch)
+    const bool lt = sj < bs;
+    close |= lt && !(sj < bs * (1.0 - 0x1p-50));
+    bs = lt ? sj : bs;
+    bi = lt ? j : bi;
+  };
+  int j = 0;
+  for (; j + 2 <= k; j += 2) {
+    const double s0 = sqd(j), s1 = sqd(j + 1);
+    step(s0, j);
+    step(s1, j + 1);
+  }
+  if (j < k) step(sqd(j), j);
+  double nd = sqrt(bs);
+  if (close) {
+    nd = sqrt(sqd(orig));
+    bi = orig;
+    for (int jj = 0; jj < k; ++jj) {
+      if (jj == orig) continue;
+      const double dj = sqrt(sqd(jj));
+      if (dj < nd) { nd = dj; bi = jj; }
+    }
+  }
+  id = bi;
+  return nd;
+}
+
+template <int DP, class TL = TileLayout<DP>>
+__device__ __forceinline__ double direct_winner(const unsigned char* tb, int r, const double* crow, int k, int d,
+                                                int orig, int& id) {
+  double x[DP];
+#pragma unroll
+  for (int q2 = 0; q2 < DP / 2; ++q2) {
+    const double2 v = *reinterpret_cast<const double2*>(tb + TL::chunk_off(r, q2, BR));
+    x[2 * q2] = v.x;
+    x[2 * q2 + 1] = v.y;
+  }
+  if (d == DP) return direct_scan<DP, true>(x, crow, k, d, orig, id);
+  return direct_scan<DP, false>(x, crow, k, d, orig, id);
+}
+
 // exact_sq_fixed<DP> (d == DP, DP in {16, 32, 64}) streamed: x from tile row r, c from a
 // crow row, eight elements at a time in the tree's own grouping (group a of every
 // 32-element block feeds z[a][*], then acc[a][l] = z[a][l] + z[a][l + 4] joins s[l] in

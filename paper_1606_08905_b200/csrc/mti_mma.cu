@@ -64,6 +64,19 @@ struct MtiMmaSmem {
   }
 };
 
+#ifndef KNB_MTI_DIRECT
+#define KNB_MTI_DIRECT 1
+#endif
+
+// warps per CTA of the direct-scan form (two CTAs per SM: 24 warps at <= 85 registers; the
+// pass is bound by the bytes it keeps in flight, profiles/README.md)
+#ifndef KNB_MTI_DIRECT_WARPS
+#define KNB_MTI_DIRECT_WARPS 8
+#endif
+template <int DP, bool HOST, bool SMALLK>
+__host__ __device__ constexpr bool mti_direct() { return KNB_MTI_DIRECT && SMALLK && !HOST && DP <= 8; }
+template <int DP, bool HOST, bool SMALLK>
+__host__ __device__ constexpr int mti_threads() { return mti_direct<DP, HOST, SMALLK>() ? 32 * KNB_MTI_DIRECT_WARPS : KNB_NT; }
 #ifndef KNB_MTI_2CTA_DP
 #define KNB_MTI_2CTA_DP 8
 #endif
@@ -74,10 +87,13 @@ struct MtiMmaSmem {
 // HOST: rows in host memory (row_gather) and/or the semi-external HBM row cache; the
 // HBM-resident instantiation keeps the plain per-lane gather
 template <int DP, bool HOST, bool SMALLK, bool LEAN>
-__global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1)
+__global__ void __launch_bounds__((mti_threads<DP, HOST, SMALLK>()), (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 : 1)
     mti_mma_kernel(const MtiArgs a) {
   using TL = TileLayout<DP, 1>;  // tiles written by cp.async only: the fragment-friendly swizzle
   constexpr int KS = DP / 4;
+  // narrow rows, few centroids (config 3): the survivors' k exact distances directly
+  // (direct_winner), no DMMA scores
+  constexpr bool DIRECT = mti_direct<DP, HOST, SMALLK>();
   extern __shared__ __align__(1024) unsigned char smem[];
   pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -173,13 +189,19 @@ __global__ void __launch_bounds__(KNB_NT, (SMALLK && DP <= KNB_MTI_2CTA_DP) ? 2 
 
   // score and update the first `cnum` queued survivors (cnum <= 32), staged in tb
   auto process = [&](const unsigned char* tb, int cnum) {
-    const Scored sc = rows_to_lanes(score_block<DP, SMALLK, LEAN, false, false, TL>(tb, bf, chn, ntile8, tolk,
-                                                                                     cmax2, lane), lane);
     const int r = lane;  // lane r handles row r from here on
     const bool valid = r < cnum;
-    int id = sc.id;
     const int orig = valid ? qorig[ring(r)] : 0;
-    const double nd = exact_winner<DP, TL>(tb, r, crow, k, d, sc.flag, id, nullptr, valid ? orig : -1);
+    int id;
+    double nd;
+    if constexpr (DIRECT) {
+      nd = direct_winner<DP, TL>(tb, r, crow, k, d, orig, id);
+    } else {
+      const Scored sc = rows_to_lanes(score_block<DP, SMALLK, LEAN, false, false, TL>(tb, bf, chn, ntile8, tolk,
+                                                                                       cmax2, lane), lane);
+      id = sc.id;
+      nd = exact_winner<DP, TL>(tb, r, crow, k, d, sc.flag, id, nullptr, valid ? orig : -1);
+    }
     const bool moved = valid && id != orig;
     // ||x||^2 only for the (few) moved rows whose signed deltas carry it
     const double sq = moved ? row_self_sq<DP, TL>(tb, r, d) : 0.0;
@@ -579,8 +601,8 @@ cudaError_t launch_w12(const MtiArgs& a, int grid, cudaStream_t s) {
   return launch_pdl(mti_w12_kernel<DP>, dim3(grid), dim3(W * 32), L.total, s, a);
 }
 
-int mti_warps_for(int DP, int k, int d, bool src = false) {
-  for (int W = KNB_WARPS; W >= 1; --W)
+int mti_warps_for(int DP, int k, int d, bool src = false, int wmax = KNB_WARPS) {
+  for (int W = wmax; W >= 1; --W)
     if (MtiMmaSmem(DP, k, d, W, src).total <= SMEM_MAX) return W;
   return 0;
 }
@@ -588,7 +610,7 @@ int mti_warps_for(int DP, int k, int d, bool src = false) {
 template <int DP, bool HOST, bool SMALLK, bool LEAN = false>
 cudaError_t launch_host(const MtiArgs& a, int grid, cudaStream_t s) {
   const bool src = HOST && a.cslot != nullptr;
-  const int W = mti_warps_for(DP, a.k, a.d, src);
+  const int W = mti_warps_for(DP, a.k, a.d, src, mti_threads<DP, HOST, SMALLK>() / 32);
   if (!W) return cudaErrorInvalidValue;
   const MtiMmaSmem L(DP, a.k, a.d, W, src);
   cudaError_t e =
