@@ -393,3 +393,38 @@ def test_skewed_row_order_matches_oracle(mode):
     assert max(s.skips for s in got.iterations) > 0.25 * ms.shape[0]  # long skipped runs did occur
     plain = kb.kmeans(m, cfg)
     assert np.array_equal(plain.assignments[order], got.assignments)
+
+
+def test_validate_bounds_catches_a_stale_row():
+    """The validator's negative case (engine.py:428-445 raises on either violation): after a
+    few pruned iterations on well-separated clusters, a row that clause 1 keeps skipping is
+    overwritten IN PLACE (the rows are attached device memory) with another cluster's
+    centroid.  The next local pass skips it again, so its stored assignment is no longer the
+    argmin and its bound is below its true distance -- knb_validate must report that row for
+    both checks, and kmeans(validate_bounds=True) semantics (an AssertionError) follow."""
+    import torch
+
+    m = kb.synth.mixture(kb.synth.MixtureSpec(20_000, 8, 6, 17, "uniform", -20, 20, 0.05, 1.0))
+    x = torch.from_numpy(m).cuda()
+    cfg = kb.EngineConfig(k=6, init="kmeanspp", seed=5, pruning=True, max_iters=40, validate_bounds=True)
+    run = kb.Lloyd(x, cfg, ignore_stop=True)
+    try:
+        for _ in range(6):
+            run.step()
+        run.local()
+        run.exchange()
+        assert run.ctx.validate() == (-1, -1)
+        run.finish()
+        means = run.ctx.centroids()[0]
+        a = run.ctx.assignments()
+        row = 4321
+        other = (int(a[row]) + 1) % 6
+        assert np.linalg.norm(means[other] - means[a[row]]) > 5.0  # separated clusters
+        x[row] = torch.from_numpy(means[other]).cuda()
+        torch.cuda.synchronize()
+        run.local()  # clause 1 skips the row (its bound still says "close to its centroid")
+        run.exchange()
+        bad_assign, bad_bound = run.ctx.validate()
+        assert bad_assign == row and bad_bound == row, (bad_assign, bad_bound)
+    finally:
+        run.close()
