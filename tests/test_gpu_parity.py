@@ -428,3 +428,26 @@ def test_validate_bounds_catches_a_stale_row():
         assert bad_assign == row and bad_bound == row, (bad_assign, bad_bound)
     finally:
         run.close()
+
+
+@pytest.mark.parametrize("mode", ["auto", "dense", "block", "exact"])
+def test_sqrt_collision_keeps_the_current_centroid(mode):
+    """scan_block compares sqrt'ed distances (pruning.py:190-203).  Here the survivor (0, 0)
+    has squared distances 1 + 2^-52 to its own centroid and exactly 1 to another one: the
+    square roots collide at 1.0, so the reference keeps the current centroid (a scan on the
+    squared values would move the row).  The centroids are fixed points of the update, the
+    third one keeps clause 1 from skipping the row; the direct-scan kernel (rows of <= 8
+    doubles, k <= 16) must take its sqrt-domain path."""
+    e = 2.0 ** -26
+    x = np.array([[0, 0], [2, 2 * e]] + [[-1, 0]] * 4 + [[1, 1.5]] * 4, dtype=np.float64)
+    init = np.array([[1, e], [-1, 0], [1, 1.5]])
+    d0 = x[0] - init[0]
+    assert float(d0 @ d0) > 1.0 and float(np.sqrt(d0 @ d0)) == 1.0
+    want = O.lloyd(x, 3, init="given", initial=init, pruning=True, max_iters=10)
+    assert want.n_iterations == 2 and list(want.assignments[:2]) == [0, 0]
+    got = kb.kmeans(x, kb.EngineConfig(k=3, init="given", initial_centroids=init, pruning=True, max_iters=10,
+                                       mti_scan=mode))
+    assert got.n_iterations == want.n_iterations
+    assert np.array_equal(got.assignments, want.assignments)
+    for a, b in zip(got.iterations, want.iterations):
+        assert (a.reassignments, a.skips) == (b.reassignments, b.skips)
