@@ -123,12 +123,17 @@ __device__ __forceinline__ void load_block(const CUtensorMap* tmap, uint64_t* ba
 #define KNB_DENSE_W12_THREADS 384
 #endif
 // ONE (k <= 8): the scorer's single-tile form (half the DMMAs of a padded tile pair)
+#ifndef KNB_DENSE_DIRECT
+#define KNB_DENSE_DIRECT 1
+#endif
 template <int DP, bool SMALLK, bool W12 = false, bool ONE = false>
 __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK && DP <= KNB_DENSE_2CTA_DP) ? 2 : 1)
     dense_mma_kernel(const __grid_constant__ CUtensorMap tmap, const DenseArgs a) {
   using TL = TileLayout<DP>;
   constexpr int KS = DP / 4;         // k-steps of 4 dims
   constexpr int NS = stages_for(DP, W12);
+  // narrow rows, few centroids (config 3's shape): rows ranked by the exact recipe directly
+  constexpr bool DIRECT = KNB_DENSE_DIRECT && SMALLK && !W12 && DP <= 8;
   extern __shared__ __align__(1024) unsigned char smem[];
   pdl_enter();
   if (a.ctrl->stop && !a.ctrl->ignore_stop) return;
@@ -260,17 +265,23 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
       skips += (valid && !live) ? 1 : 0;
       const unsigned lmask = __ballot_sync(0xffffffffu, live);
       if (lmask) {
+        int nid;
+        double nd, sq = 0.0;
+        if constexpr (DIRECT) {
+          nd = direct_winner<DP, TL>(tb, my_r, crow, k, d, live ? aa : 0, nid);
+          if (live && nid != aa) sq = row_self_sq<DP>(tb, my_r, d);
+        } else {
         Scored sc = score_block<DP, SMALLK, W12, W12, false, TL, ONE>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2,
                                                                      lane);
         if constexpr (W12) sc = rows_to_lanes(sc, lane);
-        int nid = sc.id;
-        double nd, sq = 0.0;
+        nid = sc.id;
         if constexpr (W12) {
           nd = exact_winner_stream<DP>(tb, my_r, crow, k, sc.flag, nid, live ? aa : -1);
           if (live && nid != aa) sq = exact_sq_stream<DP, true>(tb, my_r, nullptr);
         } else {
           nd = exact_winner<DP>(tb, my_r, crow, k, d, sc.flag, nid, nullptr, live ? aa : -1);
           if (live && nid != aa) sq = row_self_sq<DP>(tb, my_r, d);
+        }
         }
         if (live) {
           a.upper[row] = nd;
@@ -285,11 +296,20 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
                                              lane);
       }
     } else if (!labels) {
+      double nd2;
+      if constexpr (DIRECT) {
+        // narrow rows, few centroids: the k exact distances directly (direct_winner)
+        const double nd = direct_winner<DP, TL, false>(tb, my_r, crow, k, d, -1, id, a.mti_seed ? &my_sq : nullptr);
+        nd2 = nd * nd;
+        if (a.mti_seed && valid) {
+          a.upper[row] = nd;
+          a.tight[row] = 1;
+        }
+      } else {
       Scored sc = score_block<DP, SMALLK, W12, W12, false, TL, ONE>(tb, W12 ? crow : bf, chn, ntile8, tolk, cmax2,
                                                                    lane);
       if constexpr (W12) sc = rows_to_lanes(sc, lane);
       id = sc.id;
-      double nd2;
       if (sc.flag || a.mti_seed) {
         // exact recipe: near-tie re-rank, or the MTI bound seed (engine.py:305-308)
         double nd;
@@ -307,6 +327,7 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
       } else {
         // certified winner: WCSS term from the norm form ||x||^2 - 2 s (rounding ~1e-16 ||x||^2)
         nd2 = fmax(sc.xn2 - 2.0 * sc.best, 0.0);
+      }
       }
       old = valid ? old_raw : -1;
       if (valid) {

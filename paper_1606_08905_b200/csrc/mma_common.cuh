@@ -345,7 +345,9 @@ __device__ __forceinline__ double exact_winner(const unsigned char* tb, int r, c
 // collide -- sends the row through the sqrt-domain scan.  Every lane reads the same
 // centroid (shared-memory broadcast).  Returns the winner's distance; id = the winner.
 // FULL: d == DP, the tree's shape is known at compile time (decided once, outside the scan)
-template <int DP, bool FULL>
+// HAS_ORIG: pruned passes (scan_block's rule above); false: full passes
+// (nearest_block_into, distance.py:106-116: ascending ids, strict <, the lowest id wins a tie)
+template <int DP, bool FULL, bool HAS_ORIG>
 __device__ __forceinline__ double direct_scan(const double (&x)[DP], const double* crow, int k, int d, int orig,
                                               int& id) {
   auto sqd = [&](int j) {
@@ -354,8 +356,12 @@ __device__ __forceinline__ double direct_scan(const double (&x)[DP], const doubl
     if constexpr (FULL) return exact_sq_fixed<DP>(x, cj);
     else return exact_sq<DP>(x, cj, d);
   };
-  double bs = sqd(orig);
-  int bi = orig;
+  double bs = CUDART_INF;
+  int bi = 0;
+  if constexpr (HAS_ORIG) {
+    bs = sqd(orig);
+    bi = orig;
+  }
   bool close = false;
   // branch-free (selects), two centroids' distance chains in flight
   auto step = [&](double sj, int j) {  // (j == orig repeats bs bit for bit: no switch)
@@ -373,10 +379,10 @@ __device__ __forceinline__ double direct_scan(const double (&x)[DP], const doubl
   if (j < k) step(sqd(j), j);
   double nd = sqrt(bs);
   if (close) {
-    nd = sqrt(sqd(orig));
-    bi = orig;
+    nd = HAS_ORIG ? sqrt(sqd(orig)) : CUDART_INF;
+    bi = HAS_ORIG ? orig : 0;
     for (int jj = 0; jj < k; ++jj) {
-      if (jj == orig) continue;
+      if (HAS_ORIG && jj == orig) continue;
       const double dj = sqrt(sqd(jj));
       if (dj < nd) { nd = dj; bi = jj; }
     }
@@ -385,9 +391,10 @@ __device__ __forceinline__ double direct_scan(const double (&x)[DP], const doubl
   return nd;
 }
 
-template <int DP, class TL = TileLayout<DP>>
+// sq_out: also ||x||^2 by the exact recipe (row_sqnorms, the pruned run's first pass)
+template <int DP, class TL = TileLayout<DP>, bool HAS_ORIG = true>
 __device__ __forceinline__ double direct_winner(const unsigned char* tb, int r, const double* crow, int k, int d,
-                                                int orig, int& id) {
+                                                int orig, int& id, double* sq_out = nullptr) {
   double x[DP];
 #pragma unroll
   for (int q2 = 0; q2 < DP / 2; ++q2) {
@@ -395,8 +402,9 @@ __device__ __forceinline__ double direct_winner(const unsigned char* tb, int r, 
     x[2 * q2] = v.x;
     x[2 * q2 + 1] = v.y;
   }
-  if (d == DP) return direct_scan<DP, true>(x, crow, k, d, orig, id);
-  return direct_scan<DP, false>(x, crow, k, d, orig, id);
+  if (sq_out) *sq_out = exact_sq<DP>(x, Zero{}, d);
+  if (d == DP) return direct_scan<DP, true, HAS_ORIG>(x, crow, k, d, orig, id);
+  return direct_scan<DP, false, HAS_ORIG>(x, crow, k, d, orig, id);
 }
 
 // exact_sq_fixed<DP> (d == DP, DP in {16, 32, 64}) streamed: x from tile row r, c from a
