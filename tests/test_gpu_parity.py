@@ -451,3 +451,29 @@ def test_sqrt_collision_keeps_the_current_centroid(mode):
     assert np.array_equal(got.assignments, want.assignments)
     for a, b in zip(got.iterations, want.iterations):
         assert (a.reassignments, a.skips) == (b.reassignments, b.skips)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_direct_scan_shapes_match_oracle(seed):
+    """Rows of <= 8 doubles with k <= 16 (the direct exact-recipe scan of the dense and the
+    compacted MTI kernels) on random shapes against the oracle: mixtures, and integer
+    lattices whose exact ties exercise scan_block's keep-the-current-centroid rule and the
+    full pass's lowest-id rule (pruning.py:174-203, distance.py:106-116)."""
+    rng = np.random.default_rng(4100 + seed)
+    n = int(rng.integers(200, 12000))
+    d = int(rng.integers(1, 9))
+    k = int(rng.integers(1, 17))
+    if seed % 2:
+        m = rng.integers(-3, 4, size=(n, d)).astype(np.float64)  # lattice: many exact ties
+    else:
+        m = kb.synth.mixture(kb.synth.MixtureSpec(n, d, max(2, k // 2), 77 + seed, "uniform", -4, 4, 0.8, 1.0))
+    pruning = seed % 3 != 2
+    for mode in (("auto", "dense", "block") if pruning else ("auto",)):
+        got = kb.kmeans(m, kb.EngineConfig(k=k, init="forgy", seed=seed, pruning=pruning, max_iters=15,
+                                           mti_scan=mode))
+        want = O.lloyd(m, k, init="forgy", seed=seed, pruning=pruning, max_iters=15)
+        assert got.n_iterations == want.n_iterations, (n, d, k, mode)
+        assert np.array_equal(got.assignments, want.assignments), (n, d, k, mode)
+        for a, b in zip(got.iterations, want.iterations):
+            assert (a.reassignments, a.skips) == (b.reassignments, b.skips), (n, d, k, mode)
+        np.testing.assert_allclose(got.centroids.means, want.means, rtol=1e-9, atol=1e-12)
