@@ -20,6 +20,8 @@ the device's own stats rows.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import contextlib
+import sys
 import time
 from dataclasses import dataclass, field
 
@@ -156,6 +158,28 @@ class KmeansResult:
     @property
     def n_iterations(self) -> int:
         return len(self.iterations)
+
+
+@contextlib.contextmanager
+def _phase(name: str):
+    """NVTX range around a host-side phase of a run ("knb:upload", "knb:init", "knb:iterate",
+    "knb:results"), for nsys / ncu --nvtx timelines.  Only when the caller's process has
+    torch loaded with CUDA up (the numpy-only path never imports torch); a no-op otherwise."""
+    torch = sys.modules.get("torch")
+    nv = None
+    if torch is not None:
+        try:
+            nv = torch.cuda.nvtx if torch.cuda.is_initialized() else None
+        except Exception:
+            nv = None
+    if nv is None:
+        yield
+        return
+    nv.range_push(name)
+    try:
+        yield
+    finally:
+        nv.range_pop()
 
 
 def torch_stream(device: int) -> int:
@@ -367,13 +391,15 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
         exch = comm.make_exchange(ctx.exchange_len(), device)
         if exch is not None:
             ctx.set_exchange(exch.data_ptr(), exch.numel())
-        _attach_rows(ctx, host, dev, cfg.host_rows)
-        bad = ctx.first_nonfinite_row()
+        with _phase("knb:upload"):
+            _attach_rows(ctx, host, dev, cfg.host_rows)
+            bad = ctx.first_nonfinite_row()
         bad_global = comm.allreduce_min_int(row_lo + bad if bad >= 0 else n)
         if bad_global < n:
             raise MatrixFormatError(f"non-finite value in row {bad_global}")
-        init_rows = device_init(ctx, comm, exch, cfg.init, k, cfg.seed, cfg.initial_centroids,
-                                n, row_lo, n_local, d)
+        with _phase("knb:init"):
+            init_rows = device_init(ctx, comm, exch, cfg.init, k, cfg.seed, cfg.initial_centroids,
+                                    n, row_lo, n_local, d)
         history = [] if cfg.collect_assignments else None
         walls: list[float] = []
         batched = comm.world == 1 and history is None and not cfg.validate_bounds
@@ -381,13 +407,15 @@ def _run(host, dev, cfg: EngineConfig, comm, device=None, n_global=None, context
                    and not cfg.validate_bounds and getattr(comm, "graph_capture", False))
         if graphed:  # stop flag on the device, one captured iteration replayed (NCCL inside)
             t0 = time.perf_counter()
-            done = _run_graphed(ctx, comm, exch, cfg)
+            with _phase("knb:iterate"):
+                done = _run_graphed(ctx, comm, exch, cfg)
             el = time.perf_counter() - t0
             walls = [el / max(done, 1)] * done
         elif batched:
             t0 = time.perf_counter()
             out_pool, out_buf = _prefetch_output(n_local)
-            done = ctx.run(cfg.batch)
+            with _phase("knb:iterate"):
+                done = ctx.run(cfg.batch)
             el = time.perf_counter() - t0
             walls = [el / max(done, 1)] * done
         else:
