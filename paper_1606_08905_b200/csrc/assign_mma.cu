@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(W12 ? KNB_DENSE_W12_THREADS : KNB_NT, (SMALLK 
     if (a.mti_filter) {
       // accumulated above
     } else if (!a.delta) {
-      accumulate_in_row_order<DP, TL, W12>(row_mask(valid, my_r), id, -1, my_sq, tb, acc, cnt, sqa, d, lane);
+      accumulate_full_rows<DP, TL, W12>(row_mask(valid, my_r), id, my_sq, tb, acc, cnt, sqa, d, lane);
     } else {
       // steady-state dense passes: running sums move by the reassigned rows only
       accumulate_in_row_order<DP, TL, W12>(row_mask(valid && id != old, my_r), id, old, 0.0, tb, acc, cnt, sqa, d,

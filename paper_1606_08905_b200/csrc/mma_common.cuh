@@ -530,6 +530,53 @@ __device__ __forceinline__ void accumulate_in_row_order(unsigned rowmask, int to
   }
 }
 
+// accumulate_in_row_order for a FULL pass (every row of the mask joins cluster `to`, nothing
+// is subtracted) over rows of 16 doubles, two rows per step: lanes 0-15 add row 2i, lanes
+// 16-31 row 2i + 1 (values, count and ||x||^2) to their rows' clusters; when the two rows
+// share a cluster the halves add one after the other.  Every sum still receives its rows in
+// ascending row order -- the same additions in the same order as the one-row walk (bit-
+// identical sums) in half the steps.  Config 4's first pass: the one-row walk, 58
+// instructions per row, was half of its 323 ms; 236 ms with this.  (Narrower rows, four
+// or eight per step, measured slower than the one-row walk at small k -- config 3: 1.92-1.98
+// vs 1.82 ms -- where rows of one step share a cluster half of the time.)
+template <int DP, class TL = TileLayout<DP>, bool IDENT = false>
+__device__ __forceinline__ void accumulate_full_rows(unsigned rowmask, int to, double sq, const unsigned char* tb,
+                                                     double* acc, double* cnt, double* sqa, int d, int lane) {
+  if constexpr (DP != 16) {
+    accumulate_in_row_order<DP, TL, IDENT>(rowmask, to, -1, sq, tb, acc, cnt, sqa, d, lane);
+  } else {
+    const int half = lane >> 4, e = lane & 15;
+    const int ee = e < d ? e : 0;
+#pragma unroll 1
+    for (int r0 = 0; r0 < BR; r0 += 2) {
+      if (((rowmask >> r0) & 3u) == 0u) continue;  // warp-uniform
+      const int r = r0 + half;
+      const bool ok = (rowmask >> r) & 1u;
+      const int src = IDENT ? r : owner_lane(r);
+      const int t = __shfl_sync(0xffffffffu, to, src);
+      const double q = __shfl_sync(0xffffffffu, sq, src);
+      const double x0 = *reinterpret_cast<const double*>(tb + TL::elem_off(r, ee, BR));
+      const int t_other = __shfl_xor_sync(0xffffffffu, t, 16);
+      const bool clash = ((rowmask >> r0) & 3u) == 3u && t == t_other;  // warp-uniform
+      auto add = [&]() {
+        if (ok && e < d) acc[t * d + e] += x0;
+        if (ok && e == 0) {
+          cnt[t] += 1.0;
+          sqa[t] += q;
+        }
+      };
+      if (!clash) {
+        add();
+      } else {
+        if (half == 0) add();
+        __syncwarp();
+        if (half == 1) add();
+      }
+      __syncwarp();  // the next step's halves may touch the same sums from other lanes
+    }
+  }
+}
+
 // Bit r set when the lane owning row r (owner_lane(r)) passes `pred`.
 __device__ __forceinline__ unsigned row_mask(bool pred, int my_row) {
   return __reduce_or_sync(0xffffffffu, pred ? (1u << my_row) : 0u);
