@@ -547,22 +547,37 @@ __device__ __forceinline__ void accumulate_full_rows(unsigned rowmask, int to, d
   } else {
     const int half = lane >> 4, e = lane & 15;
     const int ee = e < d ? e : 0;
+    // step i's cluster ids, ||x||^2 and row values are fetched while step i - 1 adds (the
+    // tile and the lanes' results are read-only here; only the sums carry a dependence)
+    struct Step {
+      int t, t_other;
+      double q, x0;
+    };
+    auto fetch = [&](int r0) {
+      const int r = (r0 < BR ? r0 : 0) + half;
+      const int src = IDENT ? r : owner_lane(r);
+      Step s;
+      s.t = __shfl_sync(0xffffffffu, to, src);
+      s.q = __shfl_sync(0xffffffffu, sq, src);
+      s.x0 = *reinterpret_cast<const double*>(tb + TL::elem_off(r, ee, BR));
+      s.t_other = __shfl_xor_sync(0xffffffffu, s.t, 16);
+      return s;
+    };
+    Step nx = fetch(0);
 #pragma unroll 1
     for (int r0 = 0; r0 < BR; r0 += 2) {
-      if (((rowmask >> r0) & 3u) == 0u) continue;  // warp-uniform
-      const int r = r0 + half;
-      const bool ok = (rowmask >> r) & 1u;
-      const int src = IDENT ? r : owner_lane(r);
-      const int t = __shfl_sync(0xffffffffu, to, src);
-      const double q = __shfl_sync(0xffffffffu, sq, src);
-      const double x0 = *reinterpret_cast<const double*>(tb + TL::elem_off(r, ee, BR));
-      const int t_other = __shfl_xor_sync(0xffffffffu, t, 16);
-      const bool clash = ((rowmask >> r0) & 3u) == 3u && t == t_other;  // warp-uniform
+      const Step c = nx;
+      nx = fetch(r0 + 2);
+      const unsigned two = (rowmask >> r0) & 3u;
+      if (two == 0u) continue;  // warp-uniform
+      const bool ok = (two >> half) & 1u;
+      const int t = c.t;
+      const bool clash = two == 3u && t == c.t_other;  // warp-uniform
       auto add = [&]() {
-        if (ok && e < d) acc[t * d + e] += x0;
+        if (ok && e < d) acc[t * d + e] += c.x0;
         if (ok && e == 0) {
           cnt[t] += 1.0;
-          sqa[t] += q;
+          sqa[t] += c.q;
         }
       };
       if (!clash) {
