@@ -43,7 +43,7 @@
 //
 // Kernel shape (one CTA per SM, persistent over 128-row tiles, static schedule):
 //   warp 0      TMA producer: f64 row tiles (128 rows, SWIZZLE_128B / 64B) through an
-//               NX-stage ring, tiles PF ahead prefetched into L2
+//               NX-stage ring (five stages at c4), tiles PF ahead prefetched into L2
 //   warp 1      TMEM allocation (four 128-column accumulators) and the single-thread
 //               UMMA issuer (tile i into accumulator i % 4)
 //   warps 2-3   converters (NCONV): f64 -> (x_hi, x_lo) TF32 operand tile + the norm
@@ -128,8 +128,11 @@ constexpr int NA = KNB_TCX_NA;                 // operand stages
 #define KNB_TCX_ABL 0
 #endif
 
+// f64 stages at most.  Five, not the six that fit: 16 KB less shared memory moves the
+// carve-out from 228 to 196 KB, i.e. 60 KB of L1 instead of 28 KB for the state loads and
+// stores (measured at c4: 6 -> 45.5, 5 -> 45.0, 4 -> 46.1 ms per iteration)
 #ifndef KNB_TCX_NXMAX
-#define KNB_TCX_NXMAX 6
+#define KNB_TCX_NXMAX 5
 #endif
 constexpr int NE = 8;                          // E(x) ring (tiles), indexed by tile & 7
 constexpr int TCOLS = 128;                     // TMEM columns per accumulator buffer
@@ -280,6 +283,11 @@ __device__ __forceinline__ void for_groups(F&& f) {
   for_groups_impl(f, std::make_integer_sequence<int, NG>{});
 }
 
+// independent add-min chains of the second-smallest search (measured at c4: 2 -> 51.2,
+// 4 -> 47.5, 8 -> 45.5, 16 -> 47.1 ms per iteration)
+#ifndef KNB_TCX_CHAINS
+#define KNB_TCX_CHAINS 8
+#endif
 template <int J0, int W, int E = 0>
 __device__ __forceinline__ void pack_keys(const uint32_t (&v)[16], uint32_t mask, int (&key)[W]) {
   if constexpr (E < W) {
@@ -302,10 +310,16 @@ __device__ __forceinline__ void min2_keys(const int (&key)[W], int& gm, int& g2)
     gm = min(min(m0, m1), min(key[6], key[7]));
   }
   const uint32_t off = (uint32_t)(-gm - 1);
-  uint32_t c[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  constexpr int CH = KNB_TCX_CHAINS;  // independent add-min chains
+  uint32_t c[CH];
 #pragma unroll
-  for (int e = 0; e < W; ++e) c[e & 3] = min((uint32_t)key[e] + off, c[e & 3]);
-  g2 = (int)((uint32_t)gm + 1u + min(min(c[0], c[1]), min(c[2], c[3])));
+  for (int i = 0; i < CH; ++i) c[i] = 0xFFFFFFFFu;
+#pragma unroll
+  for (int e = 0; e < W; ++e) c[e % CH] = min((uint32_t)key[e] + off, c[e % CH]);
+  uint32_t cm = c[0];
+#pragma unroll
+  for (int i = 1; i < CH; ++i) cm = min(cm, c[i]);
+  g2 = (int)((uint32_t)gm + 1u + cm);
 }
 
 template <int XD, int NG, int LAST>
